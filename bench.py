@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the Lightning-2 hot path (fwd+bwd) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's configuration): the
+TransNormerLLM-400M attention shape B=8, H=16, d=dv=64, bf16, one step = one
+forward + backward pass of all heads at seq_len N (default 65536, the top of
+the 1K-64K sweep; every input tensor is 1 GiB, far larger than the 126 MB L2,
+so no flush is needed between steps). The full 1K-64K sweep is measured in
+the same run and reported under "sweep". Inputs are synthetic
+(torch.rand * 2 - 1), decay lam_h = exp(-2^(-8(h+1)/H)).
+
+Multi-GPU (torchrun): each rank runs its own B=8 batch (batch x head sharding,
+no collective on the data path, "scaling": "weak"); time = max over ranks.
+
+--impl reference: the reference's CPU algorithm (the oracle port of
+pkg/src/tila/kernel.py, numpy/OpenBLAS) on all host cores of rank 0, over a
+bounded sample of the same workload, extrapolated to the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd+bwd tokens/s (B=8,H=16,d=64 bf16, 1K-64K sweep)"
+UNIT = "tokens/s"
+
+
+def alibi_decay(H: int) -> list[float]:
+    return [math.exp(-(2.0 ** (-8.0 * (h + 1) / H))) for h in range(H)]
+
+
+def canonical_flops(N, d, dv):
+    """F_fwd = N[2*64(d+dv) + 4 d dv], F_bwd = N[2*64(3d+2dv) + 10 d dv]."""
+    return N * (2 * 64 * (d + dv) + 4 * d * dv), N * (2 * 64 * (3 * d + 2 * dv) + 10 * d * dv)
+
+
+def canonical_bytes(N, d, dv, e=2):
+    """Compulsory HBM bytes: fwd e*N*(2d+2dv), bwd e*N*(4d+3dv) per (b, h)."""
+    return e * N * (2 * d + 2 * dv), e * N * (4 * d + 3 * dv)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per launch of the forward F kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            j = json.loads(p.read_text())
+            return j.get("fwd_dram_bytes_per_launch"), j
+        except Exception:
+            pass
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for s in self.samples:
+            try:
+                util = float(s[6])
+                if util > 0:
+                    sm.append(float(s[0]))
+                mx = float(s[1])
+                for n, flag in zip(names, s[2:6]):
+                    if flag.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU side
+def _cpu_head_task(args):
+    n, d, seed, lam = args
+    import numpy as np
+
+    from oracle import tila_port as port
+
+    rng = np.random.default_rng(seed)
+    q, k, v, do = (rng.uniform(-1, 1, (n, d)).astype(np.float32) for _ in range(4))
+    t0 = time.perf_counter()
+    port.tiled_forward(q, k, v, lam, 64)
+    port.tiled_backward(q, k, v, do, lam, 64)
+    return time.perf_counter() - t0
+
+
+def cpu_reference(n: int, d: int, heads_total: int, tokens_per_step: int, sample_heads: int,
+                  reps: int = 1):
+    """Time the reference algorithm (oracle port, fp32, block 64) per head on
+    all host cores; extrapolate to the full B*H workload."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cores = len(os.sched_getaffinity(0))
+    sample_heads = max(sample_heads, cores)
+    decay = alibi_decay(16)
+    tasks = [(n, d, 1000 + i, decay[i % 16]) for i in range(sample_heads)]
+    ctx = mp.get_context("spawn")
+    with cf.ProcessPoolExecutor(max_workers=cores, mp_context=ctx) as ex:
+        list(ex.map(_cpu_head_task, tasks[:cores]))  # warm-up
+        walls = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(_cpu_head_task, tasks))
+            walls.append(time.perf_counter() - t0)
+    wall = statistics.median(walls)
+    t_full = wall * heads_total / sample_heads
+    return {"value": tokens_per_step / t_full, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{sample_heads} heads x N={n} d={d} fp32 fwd+bwd (tila block loop, block=64), "
+                      f"{cores} processes, median of {reps}; extrapolated x{heads_total / sample_heads:.1f} "
+                      f"to B*H={heads_total}",
+            "sample_wall_s": wall}
+
+
+# ------------------------------------------------------------------ GPU side
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--dim", type=int, default=64)
+    ap.add_argument("--seq-len", type=int, default=65536)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample-heads", type=int, default=48)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    B, H, N, D = args.batch, args.heads, args.seq_len, args.dim
+    config = {"workload": "TransNormerLLM-400M attention (BASELINE configs[1]) fwd+bwd",
+              "batch_per_gpu": B, "global_batch": B * world, "heads": H, "head_dim": D,
+              "seq_len": N, "decay": "alibi-style exp(-2^(-8(h+1)/H))",
+              "parallelism": f"bxh-shard x{world}" if world > 1 else "single",
+              "l2": "inputs (1 GiB/tensor at N=64K) larger than L2; no flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_reference(N, D, B * H * world, B * N * world, args.cpu_sample_heads, reps=max(1, min(3, args.steps)))
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "fp32", "data": "synthetic", "config": config,
+                          "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                          "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_04658_b200 as la2
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    decay = la2.decay_tensor(alibi_decay(H), H, dev)
+
+    def make(n, seed):
+        g = torch.Generator(device=dev).manual_seed(seed + 1000 * rank)
+        return [(torch.rand(B, H, n, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+                for _ in range(4)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(q, k, v, do):
+        la2.la2_forward(q, k, v, decay)
+        la2.la2_backward(q, k, v, do, decay)
+
+    def time_steps(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / steps)
+
+    hbm_peak, tc_peak, peak_src = load_peaks()
+
+    # ---------------- headline: fwd+bwd at N
+    q, k, v, do = make(N, 0)
+    clocks = ClockSampler(local_rank).start()
+    ms = time_steps(lambda: step(q, k, v, do), args.steps, max(3, args.warmup))
+    clk = clocks.stop()
+    tokens_step = B * N * world
+    value = tokens_step / (ms / 1e3)
+    ff, fb = canonical_flops(N, D, D)
+    bf, bb = canonical_bytes(N, D, D)
+    tflops = (ff + fb) * B * H * world / (ms / 1e3) / 1e12
+    t_roof = max((ff + fb) * B * H / (tc_peak * 1e12), (bf + bb) * B * H / (hbm_peak * 1e9)) * 1e3
+
+    # ---------------- dominant kernel: the F kernel, timed alone (forward launch)
+    ms_fwd = time_steps(lambda: la2.la2_forward(q, k, v, decay), max(3, args.steps), 2)
+    ms_bwd = time_steps(lambda: la2.la2_backward(q, k, v, do, decay), max(3, args.steps), 2)
+    fwd_bytes = bf * B * H
+    achieved = fwd_bytes / (ms_fwd / 1e3) / 1e9
+    traffic, _ = load_traffic()
+    roofline = {"bound": "hbm", "kernel": "la2_tc_kernel<64,fwd> (one F launch = the forward pass)",
+                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": fwd_bytes,
+                "traffic": traffic,
+                "launch_ms": ms_fwd,
+                "step": {"t_roof_ms": t_roof, "t_ms": ms, "frac_of_roof": t_roof / ms,
+                         "tflops": tflops, "frac_of_bf16_peak": tflops / tc_peak,
+                         "fwd_ms": ms_fwd, "bwd_ms": ms_bwd}}
+
+    # ---------------- sweep 1K..64K
+    sweep = []
+    if not args.no_sweep:
+        del q, k, v, do
+        torch.cuda.empty_cache()
+        n = 1024
+        while n <= N:
+            qs, ks, vs, dos = make(n, n)
+            reps = max(5, min(50, (1 << 22) // n))
+            t = time_steps(lambda: step(qs, ks, vs, dos), reps, 3)
+            fwdf, bwdf = canonical_flops(n, D, D)
+            sweep.append({"seq_len": n, "ms": t, "tokens_per_s": B * n * world / (t / 1e3),
+                          "tflops": (fwdf + bwdf) * B * H * world / (t / 1e3) / 1e12,
+                          "us_per_token": t * 1e3 / n})
+            del qs, ks, vs, dos
+            n *= 2
+        torch.cuda.empty_cache()
+        per_tok = [s["us_per_token"] for s in sweep]
+        times = [s["ms"] for s in sweep]
+        ratios = [b / a for a, b in zip(times, times[1:])]
+        flat = {"per_token_max_over_min": max(per_tok) / min(per_tok), "doubling_ratios": ratios}
+    else:
+        flat = None
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [t.cpu().pin_memory() for t in make(N, 7)]
+        h2d = sum(t.numel() * t.element_size() for t in host)
+
+        def e2e_step():
+            qh, kh, vh, doh = (t.to(dev, non_blocking=True) for t in host)
+            qh.requires_grad_(); kh.requires_grad_(); vh.requires_grad_()
+            o = la2.lightning_attn2(qh, kh, vh, decay)
+            loss = (o.float() * doh.float()).sum()
+            loss.backward()
+            return loss.item()
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_steps = max(2, min(args.steps, 5))
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+        e2e = {"value": tokens_step / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 4, "ms_per_step": t_e2e * 1e3,
+               "api": "paper_2401_04658_b200.lightning_attn2 autograd fwd+bwd, pinned host inputs"}
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        cb = cpu_reference(N, D, B * H, B * N, args.cpu_sample_heads)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": config, "tflops": tflops, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": 4 * args.steps, "clocks": clk,
+                "sweep": sweep, "flatness": flat}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,130 @@
+/*
+ * la2.h -- C ABI of the B200-native Lightning Attention-2 hot path.
+ *
+ * Drop-in boundary for the reference `tila` package (Python/NumPy,
+ * /root/reference/pkg/src/tila). Every entry point below replaces one
+ * reference function; the citation is given per function. The ABI takes
+ * plain device pointers, sizes and a cudaStream_t passed as void*; it has no
+ * torch types. All launches are asynchronous on the caller's stream; the
+ * library never allocates, frees or retains caller memory and keeps no hidden
+ * HBM workspace.
+ *
+ * Layouts (all contiguous, row-major):
+ *   q, k, dq, dk          [B, H, N, d]
+ *   v, o, dout, dv        [B, H, N, dv]
+ *   decay                 [H] float32, lambda_h in (0, 1]   (per-head decay)
+ *   states (kv, dkv)      [B, H, d, dv] float32
+ * Element type of q/k/v/o/... is selected by `dtype` (LA2_BF16 or LA2_FP32).
+ *
+ * Kernel selection is a pure function of (dtype, d, dv):
+ *   bf16, d in {64,128}, dv % 64 == 0   -> tcgen05/TMA tensor-core kernel
+ *   otherwise, d <= 128 and dv <= 128   -> SIMT fp32-accumulate kernel
+ *   anything else                       -> LA2_ERR_UNSUPPORTED (no fallback)
+ *
+ * Return value: 0 on success, a negative LA2_ERR_* code otherwise; the
+ * message of the last failure on the calling thread is la2_last_error().
+ */
+#ifndef LA2_H_
+#define LA2_H_
+
+#if defined(__GNUC__)
+#define LA2_API __attribute__((visibility("default")))
+#else
+#define LA2_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum la2_dtype { LA2_BF16 = 0, LA2_FP32 = 1 };
+
+enum la2_status {
+  LA2_OK = 0,
+  LA2_ERR_VALUE = -1,       /* bad shape / decay / pointer: Python raises ValueError   */
+  LA2_ERR_UNSUPPORTED = -2, /* shape/dtype outside the kernels' envelope: ValueError    */
+  LA2_ERR_CUDA = -3         /* launch or driver failure: Python raises RuntimeError     */
+};
+
+/* ABI version (major*100 + minor). */
+LA2_API int la2_version(void);
+
+/* Message for the most recent non-zero return on this thread ("" if none). */
+LA2_API const char* la2_last_error(void);
+
+/*
+ * Block-tiled forward pass, O = causal decayed linear attention of (q, k, v).
+ * Replaces tila.tiled_forward      (pkg/src/tila/kernel.py:122-139),
+ *          tila.chunked_forward    (pkg/src/tila/kernel.py:142-162; kv_in = caller state,
+ *                                   kv_out = returned KvState.kv),
+ *          tila.batched_forward    (pkg/src/tila/kernel.py:252-260; B*H heads, per-head decay).
+ * kv_in  (nullable): state carried in, referenced just before token 0.
+ * kv_out (nullable): final state sum_s lam^(N-1-s) k_s^T v_s + lam^N kv_in.
+ */
+LA2_API int la2_forward(const void* q, const void* k, const void* v, const float* decay, void* o,
+                const float* kv_in, float* kv_out, int B, int H, int N, int d, int dv, int dtype,
+                void* stream);
+
+/*
+ * Backward pass: gradients of sum(dout * O) with respect to q, k, v.
+ * Replaces tila.tiled_backward     (pkg/src/tila/kernel.py:165-233) and
+ *          tila.batched_backward   (pkg/src/tila/kernel.py:263-266).
+ * kv_in  (nullable): the forward kv_in (state before token 0).
+ * dkv_in (nullable): mirrored state from tokens after N-1
+ *                    (sum_{s>=N} lam^(s-N+1) q_s^T dout_s), for sequence parallelism.
+ * dkv_out(nullable): dkv folded over the whole chunk (referenced before token 0).
+ */
+LA2_API int la2_backward(const void* q, const void* k, const void* v, const void* dout,
+                 const float* decay, void* dq, void* dk, void* dv, const float* kv_in,
+                 const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dv_dim,
+                 int dtype, void* stream);
+
+/*
+ * Chunk-local forward state only (no output): S = sum_s lam^(N-1-s) k_s^T v_s.
+ * Equals the KvState.kv returned by tila.chunked_forward from a fresh state
+ * (pkg/src/tila/kernel.py:142-162). Sequence-parallel pass A.
+ */
+LA2_API int la2_chunk_state(const void* k, const void* v, const float* decay, float* s_out, int B, int H,
+                    int N, int d, int dv, int dtype, void* stream);
+
+/*
+ * Chunk-local reverse state only: T = sum_s lam^(s+1) q_s^T dout_s, the dkv of the
+ * reverse sweep of tila.tiled_backward folded over the chunk from zero
+ * (pkg/src/tila/kernel.py:207-231). Sequence-parallel backward pass A.
+ */
+LA2_API int la2_chunk_dstate(const void* q, const void* dout, const float* decay, float* t_out, int B,
+                     int H, int N, int d, int dv, int dtype, void* stream);
+
+/*
+ * Exclusive prefix (reverse=0) or suffix (reverse=1) combine of G chunk states
+ * with per-chunk decay lam^len[g]:
+ *   reverse=0: out[0] = init (or 0), out[g+1] = lam^len[g] * out[g] + states[g]
+ *   reverse=1: out[G-1] = init (or 0), out[g-1] = lam^len[g] * out[g] + states[g]
+ * states/out: [G, B*H, d, dv] fp32; lens: host array of G chunk lengths (G <= 64).
+ * The fold rule is the state update of pkg/src/tila/kernel.py:111-115 applied per chunk.
+ */
+LA2_API int la2_state_scan(const float* states, const float* decay, const float* init, float* out, int G,
+                   int B, int H, int d, int dv, const int* lens, int reverse, void* stream);
+
+/*
+ * One decode step per (b, h), in place on `state`:
+ *   state <- lam * state + k_t^T v_t ;  o_t = q_t state
+ * Replaces tila.inference_step (pkg/src/tila/reference.py:162-181, _decay_step :135-139).
+ * q,k: [B,H,d]  v,o: [B,H,dv]  state: [B,H,d,dv] fp32.
+ */
+LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const float* decay,
+                    float* state, void* o, int B, int H, int d, int dv, int dtype, void* stream);
+
+/*
+ * Self-test of the tensor-core operand layouts (not a reference replacement):
+ * D[M][N] = A[M][K] B[K][N] through the same SW128 descriptors the tcgen05
+ * kernel uses; a_mn / b_mn select MN-major staging. fp32 device buffers.
+ */
+LA2_API int la2_selftest_umma(const float* A, const float* B, float* D, int M, int N, int K,
+                              int a_mn, int b_mn, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LA2_H_ */

@@ -1,0 +1,72 @@
+"""ctypes binding of the C ABI in ``include/la2.h`` (``libla2.so``, built in-tree).
+
+There is no fallback: if the library is missing or cannot be loaded, importing
+the ops raises. Errors returned by the ABI map to ValueError (argument /
+unsupported shape, like the reference's ValueError cases in
+pkg/src/tila/reference.py:42-74) or RuntimeError (CUDA failures).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("LA2_LIB", _PKG / "libla2.so"))
+
+LA2_BF16 = 0
+LA2_FP32 = 1
+LA2_ERR_VALUE = -1
+LA2_ERR_UNSUPPORTED = -2
+LA2_ERR_CUDA = -3
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "la2_version": [],
+    "la2_last_error": [],
+    "la2_forward": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_backward": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_chunk_state": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
+    "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "la2_selftest_umma": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+}
+_RESTYPES = {"la2_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libla2.so once; raise ImportError (loudly) if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -m paper_2401_04658_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    msg = load().la2_last_error().decode(errors="replace")
+    if rc in (LA2_ERR_VALUE, LA2_ERR_UNSUPPORTED):
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg} (code {rc})")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,159 @@
+// C ABI entry points (include/la2.h): argument validation with the reference's
+// error semantics (pkg/src/tila/reference.py:42-74, kernel.py:68-70), kernel
+// selection, and the backward pass expressed as three F passes.
+#include <cstdio>
+#include <cstring>
+
+#include "la2_kernels.h"
+
+namespace la2 {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+int set_cuda_error(const char* where, cudaError_t e) {
+  std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return LA2_ERR_CUDA;
+}
+
+static bool tc_eligible(int dtype, int dk, int dv) {
+  return dtype == LA2_BF16 && (dk == 64 || dk == 128) && dv % 64 == 0 && dv >= 64 && dv <= 256;
+}
+
+static int run_f(const FArgs& a, cudaStream_t st) {
+  if (tc_eligible(a.dtype, a.dk, a.dv)) return launch_tc(a, st);
+  return launch_simt(a, st);
+}
+
+static int check_common(int B, int H, int N, int d, int dv, int dtype, const float* decay) {
+  if (B < 1 || H < 1) return set_error(LA2_ERR_VALUE, "B and H must be >= 1");
+  if (N < 1) return set_error(LA2_ERR_VALUE, "sequence length N must be >= 1");
+  if (d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "d and dv must be >= 1");
+  if (dtype != LA2_BF16 && dtype != LA2_FP32)
+    return set_error(LA2_ERR_UNSUPPORTED, "dtype must be LA2_BF16 or LA2_FP32");
+  if (decay == nullptr) return set_error(LA2_ERR_VALUE, "decay pointer is null");
+  if (!tc_eligible(dtype, d, dv) && (d > 128 || dv > 128)) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf),
+                  "unsupported shape d=%d dv=%d for dtype %s (bf16 tensor-core path: d in "
+                  "{64,128}, dv %% 64 == 0; otherwise d, dv <= 128)",
+                  d, dv, dtype == LA2_BF16 ? "bf16" : "fp32");
+    return set_error(LA2_ERR_UNSUPPORTED, buf);
+  }
+  return 0;
+}
+
+// Make this library's runtime current on the device that owns the caller's
+// stream (or, for the legacy default stream, the device of a data pointer).
+// The library links its own static cudart, so torch's current device does not
+// carry over.
+static int bind_device(void* stream, const void* ptr) {
+  int dev = -1;
+  if (stream != nullptr) {
+    cudaError_t e = cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev);
+    if (e != cudaSuccess) return set_cuda_error("cudaStreamGetDevice", e);
+  } else {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+    if (e != cudaSuccess) return set_cuda_error("cudaPointerGetAttributes", e);
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+      return set_error(LA2_ERR_VALUE, "tensor pointer is not device memory");
+    dev = at.device;
+  }
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != dev) {
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) return set_cuda_error("cudaSetDevice", e);
+  }
+  return 0;
+}
+
+}  // namespace la2
+
+using namespace la2;
+
+extern "C" {
+
+int la2_version(void) { return 100; }
+
+const char* la2_last_error(void) { return g_err; }
+
+int la2_forward(const void* q, const void* k, const void* v, const float* decay, void* o,
+                const float* kv_in, float* kv_out, int B, int H, int N, int d, int dv, int dtype,
+                void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (!q || !k || !v || !o) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  FArgs a{q, k, v, o, decay, kv_in, 0, kv_out, B, H, N, d, dv, dtype, 0};
+  return run_f(a, static_cast<cudaStream_t>(stream));
+}
+
+int la2_backward(const void* q, const void* k, const void* v, const void* dout, const float* decay,
+                 void* dq, void* dk, void* dv, const float* kv_in, const float* dkv_in,
+                 float* dkv_out, int B, int H, int N, int d, int dvd, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dvd, dtype, decay)) return rc;
+  if (int rc = check_common(B, H, N, dvd, d, dtype, decay)) return rc;
+  if (!q || !k || !v || !dout || !dq || !dk || !dv)
+    return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // dQ = F(dO, V, K): forward scan, state KV^T  (tiled_backward sweep 1, kernel.py:184-204)
+  FArgs aq{dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, dtype, 0};
+  if (int rc = run_f(aq, st)) return rc;
+  // dK = F_rev(V, dO, Q): reverse scan, state dKV^T  (sweep 2, kernel.py:207-216)
+  FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+  if (int rc = run_f(ak, st)) return rc;
+  // dV = F_rev(K, Q, dO): reverse scan, state dKV   (sweep 2, kernel.py:217-231)
+  FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
+  return run_f(av, st);
+}
+
+int la2_chunk_state(const void* k, const void* v, const float* decay, float* s_out, int B, int H,
+                    int N, int d, int dv, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (!k || !v || !s_out) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, k)) return rc;
+  FArgs a{k, k, v, nullptr, decay, nullptr, 0, s_out, B, H, N, d, dv, dtype, 0};
+  return run_f(a, static_cast<cudaStream_t>(stream));
+}
+
+int la2_chunk_dstate(const void* q, const void* dout, const float* decay, float* t_out, int B,
+                     int H, int N, int d, int dv, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (!q || !dout || !t_out) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  FArgs a{q, q, dout, nullptr, decay, nullptr, 0, t_out, B, H, N, d, dv, dtype, 1};
+  return run_f(a, static_cast<cudaStream_t>(stream));
+}
+
+int la2_state_scan(const float* states, const float* decay, const float* init, float* out, int G,
+                   int B, int H, int d, int dv, const int* lens, int reverse, void* stream) {
+  g_err[0] = 0;
+  if (!states || !decay || !out || !lens) return set_error(LA2_ERR_VALUE, "null pointer");
+  if (B < 1 || H < 1 || d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad state shape");
+  if (int rc = bind_device(stream, states)) return rc;
+  return launch_state_scan(states, decay, init, out, G, B * H, H, d, dv, lens, reverse,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int la2_decode_step(const void* q, const void* k, const void* v, const float* decay, float* state,
+                    void* o, int B, int H, int d, int dv, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (B < 1 || H < 1 || d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad decode shape");
+  if (dtype != LA2_BF16 && dtype != LA2_FP32)
+    return set_error(LA2_ERR_UNSUPPORTED, "dtype must be LA2_BF16 or LA2_FP32");
+  if (!q || !k || !v || !decay || !state || !o) return set_error(LA2_ERR_VALUE, "null pointer");
+  if (int rc = bind_device(stream, state)) return rc;
+  return launch_decode(q, k, v, decay, state, o, B, H, d, dv, dtype,
+                       static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// Internal launcher interface shared by the kernel translation units and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/la2.h"
+
+namespace la2 {
+
+// Arguments of one "F" pass (see la2_tc.cu header comment).
+//   q,k: [B,H,N,dk]   v,o: [B,H,N,dv]   (contiguous; o == nullptr -> state-only pass)
+//   kv_in / kv_out: fp32 [B,H,dk,dv] (kv_in_T: kv_in stored [B,H,dv,dk])
+struct FArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  const float* decay;
+  const float* kv_in;
+  int kv_in_T;
+  float* kv_out;
+  int B, H, N, dk, dv;
+  int dtype;
+  int reverse;
+};
+
+// Kernel-side parameter block (passed by value).
+struct FParams {
+  int N;
+  int H;
+  const float* decay;
+  const float* kv_in;
+  int kv_in_T;
+  float* kv_out;
+  int dv_total;
+};
+
+int launch_tc(const FArgs& a, cudaStream_t st);
+int launch_simt(const FArgs& a, cudaStream_t st);
+int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
+                  void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);
+int launch_state_scan(const float* chunk_states, const float* decay, const float* init,
+                      float* prefix, int G, int BH, int H, int dk, int dv, const int* lens,
+                      int reverse, cudaStream_t st);
+
+int set_error(int code, const char* msg);
+int set_cuda_error(const char* where, cudaError_t e);
+
+}  // namespace la2

@@ -1,0 +1,253 @@
+"""Torch-facing Lightning Attention-2 ops on the C ABI (``include/la2.h``).
+
+``lightning_attn2(q, k, v, decay)`` is the drop-in entry point named by the
+north star: q, k ``[B, H, N, d]``, v ``[B, H, N, dv]`` CUDA tensors (bf16 or
+fp32), ``decay`` the per-head lambda in (0, 1]. Output
+``o[b,h,t] = sum_{s<=t} lam_h^(t-s) (q_t . k_s) v_s`` -- exactly the
+reference's ``oracle_forward`` / ``tiled_forward`` (pkg/src/tila/reference.py:118-132,
+pkg/src/tila/kernel.py:122-139) applied per (b, h). No 1/sqrt(d) scale and no
+Norm(.).
+
+Every function here launches the CUDA kernels through ctypes on the current
+torch stream; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Union
+
+import torch
+
+from . import _lib
+
+DecayLike = Union[float, Sequence[float], torch.Tensor]
+
+_DTYPE_CODE = {torch.bfloat16: _lib.LA2_BF16, torch.float32: _lib.LA2_FP32}
+
+
+def _code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}; expected torch.bfloat16 or torch.float32") from None
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
+    """Per-head decay as a contiguous float32 [H] tensor on ``device``.
+
+    Host values are validated with the reference's rule lam in (0, 1]
+    (pkg/src/tila/reference.py:42-44) and raise ValueError otherwise. A CUDA
+    tensor is trusted as given (validating it would force a host sync).
+    """
+    if isinstance(decay, torch.Tensor) and decay.is_cuda:
+        d = decay.to(device=device, dtype=torch.float32).reshape(-1)
+        if d.numel() == 1:
+            d = d.expand(H)
+        if d.numel() != H:
+            raise ValueError(f"decay must have {H} entries (one per head), got {d.numel()}")
+        return d.contiguous()
+    if isinstance(decay, torch.Tensor):
+        vals = decay.detach().double().reshape(-1).tolist()
+    elif isinstance(decay, (int, float)):
+        vals = [float(decay)]
+    else:
+        vals = [float(x) for x in decay]
+    if len(vals) == 1:
+        vals = vals * H
+    if len(vals) != H:
+        raise ValueError(f"decay must have {H} entries (one per head), got {len(vals)}")
+    for lam in vals:
+        if not (0.0 < lam <= 1.0):
+            raise ValueError(f"decay rate must be in (0, 1], got {lam}")
+    return torch.tensor(vals, dtype=torch.float32, device=device)
+
+
+def _check_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+        raise ValueError("q, k, v must be 4-D [B, H, N, d] tensors")
+    if q.shape != k.shape:
+        raise ValueError(f"q and k must have the same shape, got {tuple(q.shape)} and {tuple(k.shape)}")
+    if v.shape[:3] != q.shape[:3]:
+        raise ValueError(f"v must be [B, H, N, dv] matching q's {tuple(q.shape[:3])}, got {tuple(v.shape)}")
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise ValueError("q, k, v must be CUDA tensors (there is no CPU path)")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ValueError(f"q, k, v must share a dtype, got {q.dtype}, {k.dtype}, {v.dtype}")
+    if not (q.device == k.device == v.device):
+        raise ValueError("q, k, v must be on the same device")
+    _code(q)
+    B, H, N, d = q.shape
+    return B, H, N, d, v.shape[3]
+
+
+def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name) -> Optional[torch.Tensor]:
+    if t is None:
+        return None
+    if tuple(t.shape) != (B, H, d, dv):
+        raise ValueError(f"{name} must have shape {(B, H, d, dv)}, got {tuple(t.shape)}")
+    return t.to(device=device, dtype=torch.float32).contiguous()
+
+
+# ------------------------------------------------------------------ raw passes
+def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
+                output_final_state: bool = False):
+    """One forward pass. Returns ``(o, kv_out)``; kv_out is None unless requested.
+
+    kv_in (fp32 ``[B,H,d,dv]``) is the carried state of tila.chunked_forward
+    (pkg/src/tila/kernel.py:142-162); kv_out its returned KvState.kv.
+    """
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    dec = decay_tensor(decay, H, q.device)
+    kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
+    o = torch.empty_like(v)
+    kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
+    _lib.call("la2_forward", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in), _ptr(kv_out),
+              B, H, N, d, dv, _code(q), _stream(q.device))
+    return o, kv_out
+
+
+def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, output_dkv: bool = False):
+    """Gradients of sum(d_out * O) (tila.tiled_backward, pkg/src/tila/kernel.py:165-233).
+
+    Returns ``(dq, dk, dv, dkv_out)``. dkv_in is the mirrored state from tokens
+    after the chunk (the gradient of a downstream consumer of the final state);
+    dkv_out is the mirrored state folded over the whole chunk, i.e. the gradient
+    with respect to kv_in.
+    """
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    if d_out.shape != v.shape or d_out.dtype != v.dtype:
+        raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
+    q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
+    dec = decay_tensor(decay, H, q.device)
+    kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
+    dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
+    dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dkv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_dkv else None
+    _lib.call("la2_backward", _ptr(q), _ptr(k), _ptr(v), _ptr(d_out), _ptr(dec), _ptr(dq), _ptr(dk),
+              _ptr(dvv), _ptr(kv_in), _ptr(dkv_in), _ptr(dkv_out), B, H, N, d, dv, _code(q),
+              _stream(q.device))
+    return dq, dk, dvv, dkv_out
+
+
+def chunk_state(k, v, decay: DecayLike) -> torch.Tensor:
+    """S = sum_s lam^(N-1-s) k_s^T v_s  (fp32 [B,H,d,dv]); sequence-parallel pass A."""
+    B, H, N, d, dv = _check_qkv(k, k, v)
+    k, v = k.contiguous(), v.contiguous()
+    dec = decay_tensor(decay, H, k.device)
+    out = torch.empty(B, H, d, dv, device=k.device, dtype=torch.float32)
+    _lib.call("la2_chunk_state", _ptr(k), _ptr(v), _ptr(dec), _ptr(out), B, H, N, d, dv, _code(k),
+              _stream(k.device))
+    return out
+
+
+def chunk_dstate(q, d_out, decay: DecayLike) -> torch.Tensor:
+    """T = sum_s lam^(s+1) q_s^T d_out_s (fp32 [B,H,d,dv]); SP backward pass A."""
+    B, H, N, d, dv = _check_qkv(q, q, d_out)
+    q, d_out = q.contiguous(), d_out.contiguous()
+    dec = decay_tensor(decay, H, q.device)
+    out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32)
+    _lib.call("la2_chunk_dstate", _ptr(q), _ptr(d_out), _ptr(dec), _ptr(out), B, H, N, d, dv,
+              _code(q), _stream(q.device))
+    return out
+
+
+def state_scan(states: torch.Tensor, decay: DecayLike, lens: Sequence[int],
+               init: Optional[torch.Tensor] = None, reverse: bool = False) -> torch.Tensor:
+    """Exclusive prefix (or suffix) combine of chunk states ``[G,B,H,d,dv]``."""
+    if states.dim() != 5 or states.dtype != torch.float32 or not states.is_cuda:
+        raise ValueError("states must be a CUDA float32 [G, B, H, d, dv] tensor")
+    G, B, H, d, dv = states.shape
+    if len(lens) != G:
+        raise ValueError(f"lens must have {G} entries")
+    states = states.contiguous()
+    dec = decay_tensor(decay, H, states.device)
+    if init is not None:
+        init = _state(init, B, H, d, dv, states.device, "init")
+    out = torch.empty_like(states)
+    arr = (ctypes.c_int * G)(*[int(x) for x in lens])
+    _lib.call("la2_state_scan", _ptr(states), _ptr(dec), _ptr(init), _ptr(out), G, B, H, d, dv, arr,
+              int(reverse), _stream(states.device))
+    return out
+
+
+def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.Tensor:
+    """One recurrent decode step, in place on ``state`` (fp32 ``[B,H,d,dv]``).
+
+    state <- lam*state + k_t^T v_t; returns o_t = q_t state
+    (tila.inference_step, pkg/src/tila/reference.py:162-181).
+    q_t, k_t: ``[B,H,d]``; v_t: ``[B,H,dv]``.
+    """
+    if q_t.dim() != 3 or k_t.shape != q_t.shape or v_t.dim() != 3 or v_t.shape[:2] != q_t.shape[:2]:
+        raise ValueError("decode_step expects q_t, k_t [B,H,d] and v_t [B,H,dv]")
+    B, H, d = q_t.shape
+    dv = v_t.shape[2]
+    if tuple(state.shape) != (B, H, d, dv) or state.dtype != torch.float32 or not state.is_contiguous():
+        raise ValueError(f"state must be a contiguous float32 tensor of shape {(B, H, d, dv)}")
+    if not (q_t.dtype == k_t.dtype == v_t.dtype):
+        raise ValueError("q_t, k_t, v_t must share a dtype")
+    q_t, k_t, v_t = q_t.contiguous(), k_t.contiguous(), v_t.contiguous()
+    dec = decay_tensor(decay, H, q_t.device)
+    o = torch.empty_like(v_t)
+    _lib.call("la2_decode_step", _ptr(q_t), _ptr(k_t), _ptr(v_t), _ptr(dec), _ptr(state), _ptr(o),
+              B, H, d, dv, _code(q_t), _stream(q_t.device))
+    return o
+
+
+# ------------------------------------------------------------------- autograd
+class LightningAttn2Fn(torch.autograd.Function):
+    """Autograd wrapper: saves q, k, v, decay (and the initial state) and
+    recomputes the KV state in backward -- no per-block checkpoints, matching
+    the reference's backward (pkg/src/tila/kernel.py:184-204)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, decay, initial_state, output_final_state):
+        o, kv_out = la2_forward(q, k, v, decay, kv_in=initial_state,
+                                output_final_state=output_final_state)
+        ctx.save_for_backward(q, k, v, decay, initial_state)
+        ctx.set_materialize_grads(False)
+        ctx.want_state_grad = initial_state is not None and initial_state.requires_grad
+        if kv_out is None:
+            return o
+        return o, kv_out
+
+    @staticmethod
+    def backward(ctx, d_o, *rest):
+        q, k, v, decay, initial_state = ctx.saved_tensors
+        d_final = rest[0] if rest else None
+        if d_o is None:
+            d_o = torch.zeros_like(v)
+        dq, dk, dv, dkv = la2_backward(q, k, v, d_o.to(q.dtype), decay, kv_in=initial_state,
+                                       dkv_in=d_final, output_dkv=ctx.want_state_grad)
+        return dq, dk, dv, None, dkv, None
+
+
+def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: DecayLike,
+                    initial_state: Optional[torch.Tensor] = None, output_final_state: bool = False):
+    """Causal linear attention with per-head exponential decay, on the GPU.
+
+    Args:
+      q, k: ``[B, H, N, d]``; v: ``[B, H, N, dv]`` CUDA tensors, bf16 or fp32.
+      decay: per-head lambda in (0, 1] -- float, sequence of H floats or a tensor.
+      initial_state: optional fp32 ``[B, H, d, dv]`` state carried in.
+      output_final_state: also return the fp32 final state.
+    Returns ``o`` (``[B,H,N,dv]``, input dtype), or ``(o, final_state)``.
+    """
+    _check_qkv(q, k, v)
+    dec = decay_tensor(decay, q.shape[1], q.device)
+    if initial_state is not None:
+        B, H, N, d = q.shape
+        if tuple(initial_state.shape) != (B, H, d, v.shape[3]):
+            raise ValueError(f"initial_state must have shape {(B, H, d, v.shape[3])}")
+        if initial_state.dtype != torch.float32:
+            initial_state = initial_state.float()
+    return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state))

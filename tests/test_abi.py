@@ -1,0 +1,80 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol that
+include/la2.h declares; argument validation returns the documented error
+codes before any device work. CPU only (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "la2.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"LA2_API\s+[\w\s\*]+?\b(la2_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2401_04658_b200 import build, _lib
+
+    build.build()
+    return _lib.load()
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for name in ("la2_forward", "la2_backward", "la2_chunk_state", "la2_chunk_dstate",
+                 "la2_state_scan", "la2_decode_step", "la2_last_error", "la2_version"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_python_binding_covers_header(lib):
+    from paper_2401_04658_b200 import _lib
+
+    assert set(declared_symbols()) == set(_lib.SIGNATURES)
+
+
+def test_version(lib):
+    assert lib.la2_version() == 100
+
+
+def test_validation_errors_without_device(lib):
+    from paper_2401_04658_b200 import _lib
+
+    dummy = ctypes.c_void_p(16)
+    # N = 0 -> LA2_ERR_VALUE (the reference rejects empty sequences: matrix.py:56-57)
+    rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 0, 64, 64, 0, None)
+    assert rc == _lib.LA2_ERR_VALUE
+    assert b"N must be" in lib.la2_last_error()
+    # null decay
+    rc = lib.la2_forward(dummy, dummy, dummy, None, dummy, None, None, 1, 1, 8, 64, 64, 0, None)
+    assert rc == _lib.LA2_ERR_VALUE
+    # unsupported dtype
+    rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 64, 64, 7, None)
+    assert rc == _lib.LA2_ERR_UNSUPPORTED
+    # fp32 with d > 128 is outside both kernels' envelope (no fallback)
+    rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 256, 64, 1, None)
+    assert rc == _lib.LA2_ERR_UNSUPPORTED
+    assert b"unsupported shape" in lib.la2_last_error()
+    rc = lib.la2_backward(dummy, dummy, dummy, dummy, dummy, dummy, dummy, None, None, None, None,
+                          1, 1, 8, 64, 64, 0, None)
+    assert rc == _lib.LA2_ERR_VALUE
+    lens = (ctypes.c_int * 1)(0)
+    rc = lib.la2_state_scan(dummy, dummy, None, dummy, 1, 1, 1, 4, 4, lens, 0, None)
+    assert rc != 0
+
+
+def test_check_maps_codes_to_python_errors(lib):
+    from paper_2401_04658_b200 import _lib
+
+    with pytest.raises(ValueError):
+        _lib.call("la2_forward", 16, 16, 16, 16, 16, None, None, 1, 1, 0, 64, 64, 0, None)

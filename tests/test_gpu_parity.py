@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path against the reference (golden vectors) and the
+CPU oracle port (pinned to the reference by tests/test_oracle.py).
+
+Tolerances (north star): relative error <= 1e-2 for bf16 inputs, <= 1e-4 for
+fp32 inputs, measured with the reference's metric
+max|cand - ref| / max|ref| (pkg/src/tila/verify.py:50-75) against fp64
+results computed on the same (rounded) inputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2401_04658_b200 as la2
+from paper_2401_04658_b200 import tila_api
+from oracle import tila_port as port
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2
+FP32_TOL = 1e-4
+DEV = "cuda"
+C1_DECAY = [0.5, 0.8, 0.9, 0.95, 0.99, 0.999, 0.9999, 1.0]
+
+
+def rand(shape, seed, dtype):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.rand(*shape, generator=g, dtype=torch.float64) * 2 - 1).to(dtype)
+
+
+def to64(t):
+    return t.detach().double().cpu().numpy()
+
+
+def inputs(B, H, N, d, dv, dtype, seed=0):
+    q, k = rand((B, H, N, d), seed, dtype), rand((B, H, N, d), seed + 1, dtype)
+    v, do = rand((B, H, N, dv), seed + 2, dtype), rand((B, H, N, dv), seed + 3, dtype)
+    return q, k, v, do
+
+
+def rel(got, ref):
+    return port.rel_err(to64(got) if isinstance(got, torch.Tensor) else got, ref)
+
+
+def gpu(*ts):
+    return [t.to(DEV) for t in ts]
+
+
+# --------------------------------------------------------------- reference pin
+def test_golden_case_against_reference(golden):
+    """bf16 tensor-core path vs the reference's own fp64 outputs (golden.npz)."""
+    q, k, v, do = (torch.from_numpy(golden[f"gpu/{n}_bf16bits"]).view(torch.bfloat16).to(DEV)
+                   for n in ("q", "k", "v", "do"))
+    decay = [0.9, 0.999]
+    o, kv = la2.la2_forward(q, k, v, decay, output_final_state=True)
+    dq, dk, dv, _ = la2.la2_backward(q, k, v, do, decay)
+    errs = {n: rel(t, golden[f"gpu/{n}"].astype(np.float64))
+            for n, t in (("o", o), ("kv", kv), ("dq", dq), ("dk", dk), ("dv", dv))}
+    print("golden rel errors:", errs)
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+# ------------------------------------------------------------------- C1 config
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, FP32_TOL), (torch.bfloat16, BF16_TOL)])
+def test_c1_against_quadratic_oracle(dtype, tol):
+    """BASELINE config 0: B=1 H=8 N=2048 d=64, per-head decay, vs oracle_forward/backward."""
+    B, H, N, D = 1, 8, 2048, 64
+    q, k, v, do = inputs(B, H, N, D, D, dtype, seed=11)
+    o = la2.lightning_attn2(*gpu(q, k, v), C1_DECAY)
+    dq, dk, dv, _ = la2.la2_backward(*gpu(q, k, v, do), C1_DECAY)
+    ref_o = port.bhnd_oracle_forward(to64(q), to64(k), to64(v), C1_DECAY)
+    rq, rk, rv = port.bhnd_oracle_backward(to64(q), to64(k), to64(v), to64(do), C1_DECAY)
+    errs = {"o": rel(o, ref_o), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv, rv)}
+    print(dtype, errs)
+    assert max(errs.values()) <= tol, errs
+
+
+# ------------------------------------------------------------ tensor-core shapes
+SHAPES = [
+    # (B, H, N, d, dv)
+    (1, 2, 1, 64, 64),
+    (1, 2, 128, 64, 64),
+    (2, 3, 300, 64, 64),
+    (1, 2, 257, 128, 128),
+    (1, 2, 1000, 64, 128),
+    (1, 2, 129, 128, 64),
+    (1, 2, 4096, 128, 128),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,dv", SHAPES)
+def test_tc_forward_backward(B, H, N, d, dv):
+    q, k, v, do = inputs(B, H, N, d, dv, torch.bfloat16, seed=N + d)
+    decay = [0.5, 1.0, 0.999][:H] if H <= 3 else None
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, output_final_state=True)
+    dq, dk, dv_, _ = la2.la2_backward(*gpu(q, k, v, do), decay)
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay, block=64)
+    rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay, block=64)
+    errs = {"o": rel(o, ro), "kv": rel(kv, rkv), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv)}
+    print((B, H, N, d, dv), errs)
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_tc_forward_dv256():
+    """dv = 256 runs as four 64-column value slices."""
+    q, k, v, _ = inputs(1, 1, 777, 128, 256, torch.bfloat16, seed=77)
+    o, kv = la2.la2_forward(*gpu(q, k, v), [0.95], output_final_state=True)
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), [0.95])
+    assert max(rel(o, ro), rel(kv, rkv)) <= BF16_TOL
+
+
+@pytest.mark.parametrize("d,dv", [(4, 7), (32, 35), (64, 64), (100, 20)])
+def test_simt_fp32_shapes(d, dv):
+    q, k, v, do = inputs(1, 3, 333, d, dv, torch.float32, seed=d)
+    decay = [0.5, 0.97, 1.0]
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, output_final_state=True)
+    dq, dk, dv_, _ = la2.la2_backward(*gpu(q, k, v, do), decay)
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay, block=64)
+    rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay, block=64)
+    errs = {"o": rel(o, ro), "kv": rel(kv, rkv), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv)}
+    assert max(errs.values()) <= FP32_TOL, errs
+
+
+# --------------------------------------------------------------- state carry
+@pytest.mark.parametrize("dtype,tol", [(torch.bfloat16, BF16_TOL), (torch.float32, FP32_TOL)])
+def test_chunked_forward_ragged(dtype, tol):
+    """Ragged chunks with carried state == one-shot (kernel.py:142-162)."""
+    B, H, N, D = 1, 2, 1000, 64
+    decay = [0.9, 0.9999]
+    q, k, v, _ = inputs(B, H, N, D, D, dtype, seed=5)
+    ref_o, ref_kv = port.bhnd_forward(to64(q), to64(k), to64(v), decay)
+    parts = port.ragged_partition(N, 3)
+    state = None
+    outs = []
+    start = 0
+    for L in parts:
+        sl = slice(start, start + L)
+        o, state = la2.la2_forward(*gpu(q[:, :, sl], k[:, :, sl], v[:, :, sl]), decay, kv_in=state,
+                                   output_final_state=True)
+        outs.append(o)
+        start += L
+    assert rel(torch.cat(outs, dim=2), ref_o) <= tol
+    assert rel(state, ref_kv) <= tol
+
+
+def _suffix_dstate(q, do, decay, start):
+    """sum_{s>=start} lam^(s-start+1) q_s^T do_s per (b, h), fp64."""
+    B, H, N, d = q.shape
+    out = np.zeros((B, H, d, do.shape[3]))
+    for h in range(H):
+        w = decay[h] ** (np.arange(start, N) - start + 1.0)
+        for b in range(B):
+            out[b, h] = (q[b, h, start:] * w[:, None]).T @ do[b, h, start:]
+    return out
+
+
+@pytest.mark.parametrize("d,dv", [(64, 64), (128, 128), (64, 128)])
+def test_backward_with_carried_states(d, dv):
+    """A middle chunk's gradients from (kv_in, dkv_in) equal the full-sequence
+    gradients restricted to that chunk."""
+    B, H, N = 1, 2, 700
+    a, b = 200, 450
+    decay = [0.99, 1.0]
+    q, k, v, do = inputs(B, H, N, d, dv, torch.bfloat16, seed=9)
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
+    _, kv_in = port.bhnd_forward(Q[:, :, :a], K[:, :, :a], V[:, :, :a], decay)
+    dkv_in = _suffix_dstate(Q, DO, decay, b)
+    sl = slice(a, b)
+    dq, dk, dv_, dkv_out = la2.la2_backward(
+        *gpu(q[:, :, sl], k[:, :, sl], v[:, :, sl], do[:, :, sl]), decay,
+        kv_in=torch.from_numpy(kv_in).float().to(DEV), dkv_in=torch.from_numpy(dkv_in).float().to(DEV),
+        output_dkv=True)
+    errs = {"dq": rel(dq, rq[:, :, sl]), "dk": rel(dk, rk[:, :, sl]), "dv": rel(dv_, rv[:, :, sl]),
+            "dkv_out": rel(dkv_out, _suffix_dstate(Q, DO, decay, a))}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.bfloat16, BF16_TOL), (torch.float32, FP32_TOL)])
+def test_chunk_states_and_scan(dtype, tol):
+    """SP building blocks on one GPU: pass A states, prefix/suffix scans, pass B."""
+    B, H, d = 2, 2, 64
+    lens = [300, 128, 257, 64]
+    N = sum(lens)
+    decay = [0.995, 1.0]
+    q, k, v, do = inputs(B, H, N, d, d, dtype, seed=21)
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    ref_o, _ = port.bhnd_forward(Q, K, V, decay)
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
+    bounds = np.cumsum([0] + lens)
+    S, T = [], []
+    for g in range(len(lens)):
+        sl = slice(bounds[g], bounds[g + 1])
+        S.append(la2.chunk_state(*gpu(k[:, :, sl], v[:, :, sl]), decay))
+        T.append(la2.chunk_dstate(*gpu(q[:, :, sl], do[:, :, sl]), decay))
+        _, rs = port.bhnd_forward(Q[:, :, sl], K[:, :, sl], V[:, :, sl], decay)
+        assert rel(S[-1], rs) <= tol
+        assert rel(T[-1], _suffix_dstate(Q[:, :, sl], DO[:, :, sl], decay, 0)) <= tol
+    kv_in = la2.state_scan(torch.stack(S), decay, lens)
+    dkv_in = la2.state_scan(torch.stack(T), decay, lens, reverse=True)
+    outs, gq, gk, gv = [], [], [], []
+    for g in range(len(lens)):
+        sl = slice(bounds[g], bounds[g + 1])
+        o, _ = la2.la2_forward(*gpu(q[:, :, sl], k[:, :, sl], v[:, :, sl]), decay, kv_in=kv_in[g])
+        a, b_, c, _ = la2.la2_backward(*gpu(q[:, :, sl], k[:, :, sl], v[:, :, sl], do[:, :, sl]), decay,
+                                      kv_in=kv_in[g], dkv_in=dkv_in[g])
+        outs.append(o); gq.append(a); gk.append(b_); gv.append(c)
+    errs = {"o": rel(torch.cat(outs, 2), ref_o), "dq": rel(torch.cat(gq, 2), rq),
+            "dk": rel(torch.cat(gk, 2), rk), "dv": rel(torch.cat(gv, 2), rv)}
+    assert max(errs.values()) <= tol, errs
+
+
+# --------------------------------------------------------------------- autograd
+def test_autograd_matches_raw_and_state_grad():
+    B, H, N, D = 1, 2, 500, 64
+    decay = [0.9, 0.999]
+    q, k, v, do = inputs(B, H, N, D, D, torch.bfloat16, seed=31)
+    init = torch.randn(B, H, D, D, dtype=torch.float32) * 0.1
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    ig = init.to(DEV).requires_grad_()
+    o, fin = la2.lightning_attn2(qg, kg, vg, decay, initial_state=ig, output_final_state=True)
+    (o.float() * do.to(DEV).float()).sum().backward()
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    ref_o, ref_fin = port.bhnd_forward(Q, K, V, decay, kv_in=init.double().numpy())
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
+    # gradient w.r.t. the initial state: sum_t lam^(t+1) q_t^T do_t
+    ref_ig = _suffix_dstate(Q, DO, decay, 0)
+    # dq gets the extra term lam^(t+1) do_t init^T
+    for h in range(H):
+        w = decay[h] ** (np.arange(N) + 1.0)
+        rq[0, h] += (DO[0, h] * w[:, None]) @ init.double().numpy()[0, h].T
+    errs = {"o": rel(o, ref_o), "fin": rel(fin, ref_fin), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk),
+            "dv": rel(vg.grad, rv), "dinit": rel(ig.grad, ref_ig)}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+# ------------------------------------------------------------------------ decode
+def test_decode_golden_and_fold(golden):
+    st = torch.zeros(1, 1, 4, 3, device=DEV)
+    for t in range(8):
+        o = la2.decode_step(*(torch.from_numpy(golden[f"decode/{n}"][t]).float().reshape(1, 1, -1).to(DEV)
+                              for n in ("q", "k", "v")), [0.8], st)
+        assert port.rel_err(to64(o).ravel(), golden["decode/o"][t]) <= 1e-6
+        assert port.rel_err(to64(st)[0, 0], golden["decode/kv"][t]) <= 1e-6
+    # bf16 decode over 64 tokens == recurrent forward
+    B, H, N, D = 2, 4, 64, 128
+    q, k, v, _ = inputs(B, H, N, D, D, torch.bfloat16, seed=41)
+    decay = [0.5, 0.9, 0.99, 1.0]
+    st = torch.zeros(B, H, D, D, device=DEV)
+    outs = []
+    for t in range(N):
+        outs.append(la2.decode_step(*gpu(q[:, :, t], k[:, :, t], v[:, :, t]), decay, st))
+    ref_o, ref_kv = port.bhnd_forward(to64(q), to64(k), to64(v), decay)
+    assert rel(torch.stack(outs, 2), ref_o) <= BF16_TOL
+    assert rel(st, ref_kv) <= FP32_TOL * 10
+
+
+# ------------------------------------------------------------- tila mirror API
+def test_tila_api_kats():
+    ones = [[1.0], [1.0]]
+    assert np.allclose(tila_api.tiled_forward(ones, ones, ones, 0.5, 1).o.ravel(), [1.0, 1.5])
+    g = tila_api.tiled_backward(ones, ones, ones, ones, 0.5, 1)
+    assert np.allclose(g.dq.ravel(), [1.0, 1.5]) and np.allclose(g.dk.ravel(), [1.5, 1.0])
+    assert np.allclose(g.dv.ravel(), [1.5, 1.0])
+    st = tila_api.KvState.fresh(1, 1)
+    o, st = tila_api.inference_step([1.0], [1.0], [1.0], st, 0.5)
+    o, st = tila_api.inference_step([1.0], [1.0], [1.0], st, 0.5)
+    assert np.allclose(o, [1.5]) and st.tokens_absorbed == 2
+
+
+def test_tila_api_normative_grid():
+    """The reference's equivalence grid (verify.py:127-138, every 11th case)
+    through the tila-signature API on the GPU, fp32 tolerance."""
+    worst = 0.0
+    for (n, d, dv, block, lam, seed) in port.default_grid()[::11]:
+        q, k, v, d_out = port.case_inputs(n, d, dv, seed)
+        ref = port.oracle_forward(q, k, v, lam)
+        res = tila_api.tiled_forward(q, k, v, lam, block)
+        worst = max(worst, port.rel_err(res.o, ref))
+        g = tila_api.tiled_backward(q, k, v, d_out, lam, block)
+        go = port.oracle_backward(q, k, v, d_out, lam)
+        for a in ("dq", "dk", "dv"):
+            worst = max(worst, port.rel_err(getattr(g, a), getattr(go, a)))
+        state = tila_api.KvState.fresh(d, dv)
+        outs, start = [], 0
+        for L in port.ragged_partition(n, seed):
+            o, state = tila_api.chunked_forward(q[start:start + L], k[start:start + L], v[start:start + L],
+                                                lam, block, state)
+            outs.append(o)
+            start += L
+        worst = max(worst, port.rel_err(np.concatenate(outs), ref))
+    assert worst <= FP32_TOL, worst
+
+
+def test_tila_api_batched_per_head_decay():
+    heads = []
+    for i, lam in enumerate((0.6, 0.8, 0.9, 0.99)):
+        q, k, v, _ = port.case_inputs(20, 4, 4, 20 + i)
+        heads.append((q, k, v, lam))
+    res = tila_api.batched_forward(heads, 8)
+    for (q, k, v, lam), r in zip(heads, res):
+        assert port.rel_err(r.o, port.oracle_forward(q, k, v, lam)) <= FP32_TOL
+
+
+# ------------------------------------------------------------ large-N property
+def test_long_sequence_bf16():
+    """BASELINE sizes: N = 65536, d = 64 against the O(n) fp64 tiled oracle,
+    including lam = 1 (cumulative sum, acceptance criterion 7) and a near-1 head."""
+    B, H, N, D = 1, 2, 65536, 64
+    decay = [0.99999, 1.0]
+    q, k, v, do = inputs(B, H, N, D, D, torch.bfloat16, seed=51)
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, output_final_state=True)
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay, block=256)
+    assert rel(o, ro) <= BF16_TOL
+    assert rel(kv, rkv) <= BF16_TOL
+    dq, dk, dv_, _ = la2.la2_backward(*gpu(q, k, v, do), decay)
+    rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay, block=256)
+    errs = {"dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv)}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_unsupported_shapes_raise():
+    q = torch.zeros(1, 1, 8, 256, device=DEV, dtype=torch.float32)
+    with pytest.raises(ValueError):
+        la2.la2_forward(q, q, q, 0.9)
+    q = torch.zeros(1, 1, 8, 64, device=DEV, dtype=torch.float16)
+    with pytest.raises(ValueError):
+        la2.la2_forward(q, q, q, 0.9)
