@@ -74,15 +74,16 @@ def load_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every 20 ms through NVML while the
+    timed region runs (falls back to nvidia-smi if pynvml is unavailable)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, reasons_mask, util)
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
 
@@ -92,36 +93,30 @@ class ClockSampler:
         return self
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), get_reasons(h),
+                                     nv.nvmlDeviceGetUtilizationRates(h).gpu))
+                self._stop.wait(0.02)
+        except Exception as exc:  # pragma: no cover - reported in the JSON
+            self.error = repr(exc)
 
     def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], None, set()
-        for s in self.samples:
-            try:
-                util = float(s[6])
-                if util > 0:
-                    sm.append(float(s[0]))
-                mx = float(s[1])
-                for n, flag in zip(names, s[2:6]):
-                    if flag.lower() == "active":
-                        reasons.add(n)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        busy = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = sorted({name for s in busy for bit, name in self.REASONS.items() if s[1] & bit})
+        return {"sm_mhz": statistics.median([s[0] for s in busy]) if busy else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml"}
 
 
 # ------------------------------------------------------------------ CPU side
@@ -173,7 +168,7 @@ def cpu_reference(n: int, d: int, heads_total: int, tokens_per_step: int, sample
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=8)

@@ -470,20 +470,24 @@ template <int DK, bool REV, bool SO>
 static int launch_tc_t(const FArgs& a, cudaStream_t st) {
   using L = TcLayout<DK, SO>;
   auto kern = la2_tc_kernel<DK, REV, SO>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tc)", e);
-    attr_set = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tc)", e);
   CUtensorMap mq, mk, mv, mo;
   const int BH = a.B * a.H;
-  int rc = 0;
-  if (!SO) rc |= make_tmap(&mq, a.q, DK, a.N, BH);
-  rc |= make_tmap(&mk, a.k, DK, a.N, BH);
-  rc |= make_tmap(&mv, a.v, a.dv, a.N, BH);
-  if (!SO) rc |= make_tmap(&mo, a.o, a.dv, a.N, BH);
-  if (rc != 0) return set_error(LA2_ERR_CUDA, "cuTensorMapEncodeTiled failed (pointer alignment?)");
+  const void* ptrs[4] = {a.q, a.k, a.v, a.o};
+  CUtensorMap* maps[4] = {&mq, &mk, &mv, &mo};
+  const int cols[4] = {DK, DK, a.dv, a.dv};
+  for (int t = 0; t < 4; ++t) {
+    if (SO && (t == 0 || t == 3)) continue;
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH);
+    if (rc != 0) {
+      char buf[256];
+      std::snprintf(buf, sizeof(buf),
+                    "cuTensorMapEncodeTiled failed for %c: CUresult %d (ptr=%p cols=%d N=%d BH=%d)",
+                    "qkvo"[t], -(rc + 1000), ptrs[t], cols[t], a.N, BH);
+      return set_error(LA2_ERR_CUDA, buf);
+    }
+  }
   if (SO) { mq = mk; mo = mv; }
   FParams p;
   p.N = a.N;
@@ -495,7 +499,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st) {
   p.dv_total = a.dv;
   dim3 grid(a.dv / DVS, a.H, a.B);
   kern<<<grid, TC_THREADS, L::TOTAL, st>>>(mq, mk, mv, mo, p);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   return 0;
 }
