@@ -123,6 +123,15 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
 LA2_API int la2_selftest_umma(const float* A, const float* B, float* D, int M, int N, int K,
                               int a_mn, int b_mn, void* stream);
 
+/* Micro-benchmark of one tcgen05.mma shape (development tool): clock cycles per CTA
+ * for `iters` back-to-back K=16 MMAs; a_mode 0/1/2 = A K-major smem / MN-major smem / TMEM. */
+LA2_API int la2_bench_umma(int M, int N, int a_mode, int b_mn, int iters, int ctas, long long* out,
+                           void* stream);
+
+/* Micro-benchmark of TMEM -> register loads (development tool). */
+LA2_API int la2_bench_tmem(int warps, int iters, int batch, int ctas, long long* out, float* sink,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

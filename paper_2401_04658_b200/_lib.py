@@ -35,6 +35,8 @@ SIGNATURES: dict[str, list] = {
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_selftest_umma": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "la2_bench_umma": [_i, _i, _i, _i, _i, _i, _vp, _vp],
+    "la2_bench_tmem": [_i, _i, _i, _i, _vp, _vp, _vp],
 }
 _RESTYPES = {"la2_last_error": ctypes.c_char_p}
 

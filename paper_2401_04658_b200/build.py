@@ -29,9 +29,9 @@ def _flags() -> list[str]:
     ]
 
 
-def _compile(src: str, verbose: bool) -> Path:
-    obj = CSRC / (Path(src).stem + ".o")
-    cmd = [NVCC, *_flags(), "-c", str(CSRC / src), "-o", str(obj)]
+def _compile(src: str, verbose: bool, extra=(), tag="") -> Path:
+    obj = CSRC / (Path(src).stem + tag + ".o")
+    cmd = [NVCC, *_flags(), *extra, "-c", str(CSRC / src), "-o", str(obj)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,21 +51,24 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """Build libla2.so (or, with trace=True, the phase-trace variant libla2_trace.so)."""
+    lib = PKG / "libla2_trace.so" if trace else LIB
+    if not trace and not force and not _stale():
         return LIB
+    extra, tag = (["-DLA2_TRACE"], "_trace") if trace else ((), "")
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    tmp = LIB.with_suffix(".so.tmp")
+        objs = list(ex.map(lambda s: _compile(s, verbose, extra, tag), SOURCES))
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         o.unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -50,8 +50,23 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *slot;
+  const bool a_tmem = (a_mn == 2);
+  if (a_tmem) {
+    // A row m -> TMEM lane m, columns 128.. as packed bf16 pairs (K-major)
+    const int m = (warp & 3) * 32 + lane;
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t r[16];
+      for (int j = 0; j < 16; ++j)
+        r[j] = pack_bf16x2(A[m * K + 2 * (c0 + j)], A[m * K + 2 * (c0 + j) + 1]);
+      tmem_st16(tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 128 + c0, r);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   if (tid == 0) {
-    const uint32_t id = idesc_bf16(M, N, a_mn, b_mn);
+    const uint32_t id = idesc_bf16(M, N, a_tmem ? 0 : a_mn, b_mn);
     const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
     for (int kk = 0; kk < K / 16; ++kk) {
       uint64_t ad, bd;
@@ -59,7 +74,8 @@ __global__ void __launch_bounds__(128, 1)
       else ad = sdesc_sw128(a0 + kk * 2048, K * 128, 1024);
       if (!b_mn) bd = sdesc_sw128(b0 + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024);
       else bd = sdesc_sw128(b0 + kk * 2048, K * 128, 1024);
-      umma_bf16_ss(tbase, ad, bd, id, kk > 0);
+      if (a_tmem) umma_bf16_ts(tbase, tbase + 128 + kk * 8, bd, id, kk > 0);
+      else umma_bf16_ss(tbase, ad, bd, id, kk > 0);
     }
     umma_commit(bar);
   }
@@ -91,6 +107,7 @@ extern "C" LA2_API int la2_selftest_umma(const float* A, const float* B, float* 
   using namespace la2;
   if (!((M == 64 || M == 128) && (N == 64 || N == 128) && (K == 64 || K == 128)))
     return set_error(LA2_ERR_VALUE, "selftest: M,N in {64,128}, K in {64,128}");
+  if (a_mn == 2 && M != 128) return set_error(LA2_ERR_VALUE, "selftest: TMEM A needs M=128");
   const int smem = 65536 + 128 + 1024;
   cudaError_t e = cudaFuncSetAttribute(la2_umma_selftest_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -99,5 +116,122 @@ extern "C" LA2_API int la2_selftest_umma(const float* A, const float* B, float* 
                                                                                 a_mn, b_mn);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("selftest launch", e);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Microbenchmark: cycles per tcgen05.mma for one (M, N, A-mode, B-major) shape.
+// a_mode: 0 = A K-major smem, 1 = A MN-major smem, 2 = A from TMEM. One CTA per
+// SM issues `iters` MMAs back to back (K = 16 each) and reports clock cycles.
+namespace la2 {
+__global__ void __launch_bounds__(128, 1)
+    la2_umma_bench_kernel(int M, int N, int a_mode, int b_mn, int iters, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  for (int e = threadIdx.x; e < 65536 / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[e] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+  if (threadIdx.x < 32) tmem_alloc(slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *slot;
+  if (threadIdx.x == 0) {
+    const uint32_t id = idesc_bf16(M, N, a_mode == 1 ? 1 : 0, b_mn & 1);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
+    const uint64_t ad = a_mode == 1 ? sdesc_sw128(a0, 16384, 1024) : sdesc_sw128(a0, 16, 1024);
+    const uint64_t bd = (b_mn & 1) ? sdesc_sw128(b0, 16384, 1024) : sdesc_sw128(b0, 16, 1024);
+    const int chains = (b_mn >> 1) < 1 ? 1 : (b_mn >> 1);
+    // precomputed descriptors; 16 MMAs per unrolled group, D rotates over `chains`
+    const uint32_t d1 = tbase + (chains > 1 ? N : 0), d2 = tbase + (chains > 2 ? 2 * N : 0),
+                   d3 = tbase + (chains > 3 ? 3 * N : (chains > 1 ? N : 0));
+    const uint32_t dd[4] = {tbase, d1, chains == 3 ? d2 : (chains > 1 ? d2 : tbase), d3};
+    const uint32_t at = tbase + 256;
+    long long t0 = clock64();
+    if (a_mode == 2) {
+      for (int i = 0; i < iters; i += 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) umma_bf16_ts(dd[u & 3], at, bd, id, 1);
+      }
+    } else {
+      for (int i = 0; i < iters; i += 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) umma_bf16_ss(dd[u & 3], ad, bd, id, 1);
+      }
+    }
+    umma_commit(bar);
+    mbar_wait(bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x < 32) tmem_dealloc(tbase, 512);
+}
+}  // namespace la2
+
+extern "C" LA2_API int la2_bench_umma(int M, int N, int a_mode, int b_mn, int iters, int ctas,
+                                      long long* out, void* stream) {
+  using namespace la2;
+  const int smem = 65536 + 128 + 1024;
+  cudaError_t e = cudaFuncSetAttribute(la2_umma_bench_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error("bench attr", e);
+  la2_umma_bench_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(M, N, a_mode, b_mn,
+                                                                               iters, out);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("bench launch", e);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Microbenchmark: TMEM -> register load throughput (tcgen05.ld 32x32b.x16) with
+// `warps` warps (multiple of 4); returns cycles for `iters` loads of 16 columns
+// per warp (64 B per lane -> 2 KB per warp per load).
+namespace la2 {
+__global__ void la2_tmem_bench_kernel(int iters, int batch, long long* out, float* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = slot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  float acc = 0.f;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; i += 4) {
+    float v[4][16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      tmem_ld16(tbase + ((i + u + warp) & 31) * 16, v[u]);
+      if (batch == 1) tmem_ld_wait();
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc += v[u][e];
+  }
+  long long t1 = clock64();
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(slot, 512);
+}
+}  // namespace la2
+
+extern "C" LA2_API int la2_bench_tmem(int warps, int iters, int batch, int ctas, long long* out,
+                                      float* sink, void* stream) {
+  using namespace la2;
+  la2_tmem_bench_kernel<<<ctas, warps * 32, 0, static_cast<cudaStream_t>(stream)>>>(iters, batch,
+                                                                                    out, sink);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("tmem bench launch", e);
   return 0;
 }

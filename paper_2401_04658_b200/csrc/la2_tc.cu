@@ -8,18 +8,23 @@
 // (pkg/src/tila/kernel.py:207-231) written as a forward pass over reversed time.
 //
 // Per 128-token block i (rows t, u in [0,128), r = rows present):
-//   S      = Q_i K_i^T                                   (tcgen05, TMEM fp32)
-//   P      = bf16(S * M)   M[t][u] = lam^(t-u), u<=t     (fwd; transposed for rev)
-//   Q~     = bf16(a_t * Q_i)    a_t = lam^(t+1)  | rev: lam^(r-1-t)    (in place)
-//   K~     = bf16(c_t * K_i)    c_t = lam^(r-1-t)| rev: lam^(t+1)      (in place)
-//   O_i    = P V_i + Q~ KV_{i-1}                          (one TMEM accumulator)
-//   dKV    = K~^T V_i                                     (tcgen05)
-//   KV_i   = lam^r KV_{i-1} + dKV                         (fp32, registers)
-// The fp32 KV state never leaves the SM; its bf16 copy is the B operand of the
-// next block's Q~ KV product.
+//   S      = Q_i K_i^T                              SS-MMA  -> TMEM S[b] (fp32)
+//   P      = bf16(S * M)  M[t][u] = lam^(t-u), u<=t (rev: lam^(u-t), u>=t), written back
+//            into TMEM over S[b] (packed bf16 pairs) by the row warps
+//   O_i    = P V_i                                  TS-MMA  (A = P from TMEM)
+//   Oe_i   = Q_i KV_{i-1}                           SS-MMA  (KV as bf16 B operand)
+//   o_t    = O_i[t] + a_t Oe_i[t]    a_t = lam^(t+1) | rev: lam^(r-1-t)   (registers)
+//   K~     = bf16(c_t K_i)           c_t = lam^(r-1-t)| rev: lam^(t+1)    (state warps)
+//   dKV    = K~^T V_i                               SS-MMA  -> TMEM
+//   KV_i   = lam^r KV_{i-1} + dKV                   fp32 registers of the state warps
+// The fp32 KV state never leaves the SM.
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2-5 "row" warps (thread <-> TMEM lane <-> token row).
+// Warp roles (448 threads, one CTA per SM):
+//   warp 0     TMA producer (Q/K/V ring of NS stages)
+//   warp 1     MMA issuer (one thread) + TMEM owner
+//   warps 2-9  row warps:   thread <-> token row, two warps per TMEM lane quarter
+//              splitting the columns; S -> P, O epilogue + TMA store
+//   warps 10-13 state warps: K~ rows, dKV -> fp32 KV state -> bf16 KV operand
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -29,80 +34,82 @@
 
 namespace la2 {
 
+// Optional phase trace (build with -DLA2_TRACE): CTA (0,0,0) records clock64()
+// stamps per role / block / event into g_trace[role][block][event].
+#ifdef LA2_TRACE
+__device__ long long* g_trace = nullptr;
+constexpr int TR_MAXB = 64, TR_EV = 8;
+#define TR(role, blk, ev)                                                                        \
+  do {                                                                                           \
+    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (blk) < TR_MAXB &&  \
+        (threadIdx.x & 31) == 0)                                                                 \
+      g_trace[((role) * TR_MAXB + (blk)) * TR_EV + (ev)] = clock64();                            \
+  } while (0)
+#else
+#define TR(role, blk, ev) \
+  do {                    \
+  } while (0)
+#endif
+
 constexpr int BT = 128;        // tokens per block
 constexpr int DVS = 64;        // value columns per CTA (dv slice)
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 448;  // 14 warps
+constexpr int NROW = 8;         // row warps (2 per TMEM lane quarter)
+constexpr int W0 = 2 + NROW;    // first state warp
 constexpr int REGION = BT * 64 * 2;  // one [128][64] bf16 SW128 region = 16 KB
 
 template <int DK, bool SO>
 struct TcLayout {
-  static constexpr int NS = 2;  // Q/K/V stages
+  static constexpr int NS = (DK == 64) ? 3 : 2;   // Q/K/V stages
+  static constexpr int KTS = (DK == 64) ? 2 : 1;  // K~ buffers
+  static constexpr int OS = (DK == 64 && !SO) ? 2 : 1;  // O staging buffers
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
   static constexpr int K_BYTES = BT * DK * 2;
   static constexpr int V_BYTES = BT * DVS * 2;
-  static constexpr int P_BYTES = SO ? 0 : BT * BT * 2;
   static constexpr int KV_BYTES = SO ? 0 : DK * DVS * 2;
   static constexpr int O_BYTES = SO ? 0 : BT * DVS * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
-  static constexpr int OFF_P = OFF_V + NS * V_BYTES;
-  static constexpr int OFF_KV = OFF_P + P_BYTES;
+  static constexpr int OFF_KT = OFF_V + NS * V_BYTES;
+  static constexpr int OFF_KV = OFF_KT + KTS * K_BYTES;
   static constexpr int OFF_O = OFF_KV + KV_BYTES;
-  static constexpr int OFF_BAR = OFF_O + O_BYTES;
+  static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
   static constexpr int BAR_BYTES = 256;
   static constexpr int TOTAL = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
-  // S[2] + O[2] + dKV[2]; the state-only pass needs dKV[2] only
+  // TMEM columns: S[2] @0,128 (P aliased) | O @256 | Oe @320 | dKV @384 (state-only: dKV @0)
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
+  static constexpr uint32_t T_O = 256, T_OE = 320, T_KV = SO ? 0 : 384;
+  // barrier slots
+  static constexpr int B_FULL = 0, B_EMPTY = NS, B_SFULL = 2 * NS, B_SFREE = B_SFULL + 2,
+                       B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEMPTY = B_OFULL + 1,
+                       B_KTREADY = B_OEMPTY + 1, B_KTFREE = B_KTREADY + KTS,
+                       B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 1,
+                       B_KVREADY = B_DKVEMPTY + 1, B_COUNT = B_KVREADY + 1;
+  static_assert(B_COUNT * 8 + 16 <= BAR_BYTES, "barrier area");
+  static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
-// Barrier slots inside the barrier area.
-enum : int {
-  B_FULL = 0,      // [2] TMA -> MMA / row warps
-  B_EMPTY = 2,     // [2] MMA commit -> TMA
-  B_SFULL = 4,     // [2] S ready
-  B_SEMPTY = 6,    // [2] S consumed
-  B_OFULL = 8,     // [2] O + dKV ready
-  B_OEMPTY = 10,   // [2] O + dKV consumed
-  B_PREADY = 12,   // P, Q~, K~ written
-  B_PFREE = 13,    // P consumed by the P.V product
-  B_KVREADY = 14,  // bf16 KV state written
-  B_COUNT = 15
-};
-
-// Scale one token row (all DK columns) of a K-major SW128 tile in place.
+// Copy one token row of a K-major SW128 tile, scaled by f, into the same row of dst.
 template <int DK>
-__device__ __forceinline__ void scale_row_inplace(uint8_t* tile, int row, float f) {
+__device__ __forceinline__ void scale_row_copy(const uint8_t* src, uint8_t* dst, int row, float f) {
 #pragma unroll
   for (int reg = 0; reg < DK / 64; ++reg) {
-    uint8_t* rp = tile + reg * REGION + row * 128;
+    const uint8_t* sp = src + reg * REGION + row * 128;
+    uint8_t* dp = dst + reg * REGION + row * 128;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = (k + row) & 7;  // rotate to spread banks across the warp
-      uint4 w = *reinterpret_cast<uint4*>(rp + c * 16);
+      const int c = (k + row) & 7;  // rotate chunks to spread banks across the warp
+      uint4 w = *reinterpret_cast<const uint4*>(sp + c * 16);
       uint32_t* u = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float2 x = unpack_bf16x2(u[e]);
         u[e] = pack_bf16x2(x.x * f, x.y * f);
       }
-      *reinterpret_cast<uint4*>(rp + c * 16) = w;
+      *reinterpret_cast<uint4*>(dp + c * 16) = w;
     }
-  }
-}
-
-// Write 64 fp32 values as one bf16 SW128 row (128 bytes) of a [rows][64] region.
-__device__ __forceinline__ void store_row64_bf16(uint8_t* region, int row, const float* x) {
-  uint8_t* rp = region + row * 128;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint4 w;
-    w.x = pack_bf16x2(x[8 * c + 0], x[8 * c + 1]);
-    w.y = pack_bf16x2(x[8 * c + 2], x[8 * c + 3]);
-    w.z = pack_bf16x2(x[8 * c + 4], x[8 * c + 5]);
-    w.w = pack_bf16x2(x[8 * c + 6], x[8 * c + 7]);
-    *reinterpret_cast<uint4*>(rp + ((c ^ (row & 7)) * 16)) = w;
   }
 }
 
@@ -121,16 +128,22 @@ __device__ __forceinline__ void store_chunk16_bf16(uint8_t* region, int row, int
   }
 }
 
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 template <int DK, bool REV, bool SO>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     la2_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                   const FParams p) {
   using L = TcLayout<DK, SO>;
+  constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_COUNT);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::B_COUNT);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -141,21 +154,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nblk = (N + BT - 1) / BT;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[B_FULL + 0], 1);
-    mbar_init(&bars[B_FULL + 1], 1);
-    mbar_init(&bars[B_EMPTY + 0], 1);
-    mbar_init(&bars[B_EMPTY + 1], 1);
-    mbar_init(&bars[B_SFULL + 0], 1);
-    mbar_init(&bars[B_SFULL + 1], 1);
-    mbar_init(&bars[B_SEMPTY + 0], 4);
-    mbar_init(&bars[B_SEMPTY + 1], 4);
-    mbar_init(&bars[B_OFULL + 0], 1);
-    mbar_init(&bars[B_OFULL + 1], 1);
-    mbar_init(&bars[B_OEMPTY + 0], 4);
-    mbar_init(&bars[B_OEMPTY + 1], 4);
-    mbar_init(&bars[B_PREADY], 4);
-    mbar_init(&bars[B_PFREE], 1);
-    mbar_init(&bars[B_KVREADY], 4);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bars[L::B_FULL + s], 1);
+      mbar_init(&bars[L::B_EMPTY + s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[L::B_SFULL + b], 1);
+      mbar_init(&bars[L::B_SFREE + b], 1);
+      mbar_init(&bars[L::B_PREADY + b], NROW);
+    }
+    mbar_init(&bars[L::B_OFULL], 1);
+    mbar_init(&bars[L::B_OEMPTY], NROW);
+    for (int b = 0; b < KTS; ++b) {
+      mbar_init(&bars[L::B_KTREADY + b], 4);
+      mbar_init(&bars[L::B_KTFREE + b], 1);
+    }
+    mbar_init(&bars[L::B_DKVFULL], 1);
+    mbar_init(&bars[L::B_DKVEMPTY], 4);
+    mbar_init(&bars[L::B_KVREADY], 4);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -169,136 +185,234 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  // TMEM column map: S[2] @0,128  O[2] @256,320  dKV[2] @384,448 (state-only: dKV @0,64)
-  auto tS = [&](int b) { return tbase + b * 128; };
-  auto tO = [&](int b) { return tbase + 256 + b * 64; };
-  auto tKV = [&](int b) { return tbase + (SO ? 0 : 384) + b * 64; };
+
+  const float lam = p.decay[h];
+  // exact log2 (fast-math log2f is off by ~2^-22 absolute, which compounds over
+  // 64K tokens when lam is close to 1)
+  const float l2 = (lam >= 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       for (int i = 0; i < nblk; ++i) {
         const int blk = REV ? (nblk - 1 - i) : i;
-        const int s = i & 1;
-        if (i >= 2) mbar_wait(&bars[B_EMPTY + s], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&bars[B_FULL + s], L::STAGE_TX);
+        const int s = i % NS;
+        TR(0, i, 0);
+        if (i >= NS) mbar_wait(&bars[L::B_EMPTY + s], ((i / NS) - 1) & 1);
+        TR(0, i, 1);
+        mbar_arrive_expect_tx(&bars[L::B_FULL + s], L::STAGE_TX);
         const int row = blk * BT;
 #pragma unroll
         for (int c = 0; c < DK / 64; ++c) {
           if (!SO)
-            tma_load_3d(smem + L::OFF_Q + s * L::Q_BYTES + c * REGION, &tm_q, &bars[B_FULL + s],
-                        c * 64, row, bh);
-          tma_load_3d(smem + L::OFF_K + s * L::K_BYTES + c * REGION, &tm_k, &bars[B_FULL + s],
+            tma_load_3d(smem + L::OFF_Q + s * L::Q_BYTES + c * REGION, &tm_q,
+                        &bars[L::B_FULL + s], c * 64, row, bh);
+          tma_load_3d(smem + L::OFF_K + s * L::K_BYTES + c * REGION, &tm_k, &bars[L::B_FULL + s],
                       c * 64, row, bh);
         }
-        tma_load_3d(smem + L::OFF_V + s * L::V_BYTES, &tm_v, &bars[B_FULL + s], slice * DVS, row,
-                    bh);
+        tma_load_3d(smem + L::OFF_V + s * L::V_BYTES, &tm_v, &bars[L::B_FULL + s], slice * DVS,
+                    row, bh);
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
-      constexpr uint32_t ID_O = idesc_bf16(128, DVS, 0, 1);   // P/Q~ (K-major) x V/KV (MN-major)
-      constexpr uint32_t ID_KV = idesc_bf16(DK, DVS, 1, 1);   // K~^T (MN-major) x V (MN-major)
-      const uint32_t sQ = smem_u32(smem + L::OFF_Q), sK = smem_u32(smem + L::OFF_K);
-      const uint32_t sV = smem_u32(smem + L::OFF_V), sP = smem_u32(smem + L::OFF_P);
-      const uint32_t sKV = smem_u32(smem + L::OFF_KV);
+    // The whole warp walks the schedule (converged barrier waits); one lane issues.
+    constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K (K-major)
+    constexpr uint32_t ID_O = idesc_bf16(128, DVS, 0, 1);  // P/Q (K-major) x V/KV (MN-major)
+    constexpr uint32_t ID_KV = idesc_bf16(DK, DVS, 1, 1);  // K~^T (MN-major) x V (MN-major)
+    const bool leader = (lane == 0);
+    const uint32_t tO = tbase + L::T_O, tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
+    // descriptor bases (start address is in 16-byte units in the low bits)
+    const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
+    const uint64_t dK0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
+    const uint64_t dV0 = sdesc_sw128(smem_u32(smem + L::OFF_V), REGION, 1024);
+    const uint64_t dKT0 = sdesc_sw128(smem_u32(smem + L::OFF_KT), REGION, 1024);
+    const uint64_t dKV0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), DK * 128, 1024);
+    auto adv = [](uint64_t d, uint32_t bytes) { return d + static_cast<uint64_t>(bytes >> 4); };
 
-      auto issue_S = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(&bars[B_FULL + s], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&bars[B_SEMPTY + s], ((j >> 1) - 1) & 1);
-        tc_fence_after();
+    auto issue_S = [&](int j) {
+      const int s = j % NS, b = j & 1;
+      mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+      if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
 #pragma unroll
         for (int kk = 0; kk < DK / 16; ++kk) {
           const uint32_t off = (kk >> 2) * REGION + (kk & 3) * 32;
-          umma_bf16_ss(tS(s), sdesc_sw128(sQ + s * L::Q_BYTES + off, 16, 1024),
-                       sdesc_sw128(sK + s * L::K_BYTES + off, 16, 1024), ID_S, kk > 0);
+          umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
         }
-        umma_commit(&bars[B_SFULL + s]);
-      };
+        umma_commit(&bars[L::B_SFULL + b]);
+      }
+      __syncwarp();
+    };
 
-      if (!SO) issue_S(0);
-      for (int i = 0; i < nblk; ++i) {
-        const int s = i & 1;
-        if (!SO) {
-          if (i + 1 < nblk) issue_S(i + 1);
-        } else {
-          mbar_wait(&bars[B_FULL + s], (i >> 1) & 1);
-        }
-        mbar_wait(&bars[B_PREADY], i & 1);
-        if (i >= 2) mbar_wait(&bars[B_OEMPTY + s], ((i >> 1) - 1) & 1);
+    if (!SO) issue_S(0);
+    for (int i = 0; i < nblk; ++i) {
+      const int s = i % NS, b = i & 1, kt = i % KTS;
+      const uint64_t v = adv(dV0, s * L::V_BYTES);
+      if (!SO) {
+        TR(1, i, 0);
+        if (i + 1 < nblk) issue_S(i + 1);
+        TR(1, i, 1);
+        // O = P V  (A = P in TMEM over S[b], K = 128 tokens)
+        mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
+        TR(1, i, 2);
+        if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
+        TR(1, i, 3);
         tc_fence_after();
-        if (!SO) {
-          // O = P V   (K = 128 tokens)
+        if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk) {
-            umma_bf16_ss(tO(s),
-                         sdesc_sw128(sP + (kk >> 2) * REGION + (kk & 3) * 32, 16, 1024),
-                         sdesc_sw128(sV + s * L::V_BYTES + kk * 2048, REGION, 1024), ID_O,
+          for (int kk = 0; kk < BT / 16; ++kk)
+            umma_bf16_ts(tO, tbase + b * 128 + (kk >> 2) * 64 + (kk & 3) * 8, adv(v, kk * 2048),
+                         ID_O, kk > 0);
+          umma_commit(&bars[L::B_SFREE + b]);
+        }
+        __syncwarp();
+        // Oe = Q KV_{i-1}  (K = DK)
+        mbar_wait(&bars[L::B_KVREADY], i & 1);
+        TR(1, i, 4);
+        tc_fence_after();
+        if (leader) {
+          const uint64_t q = adv(dQ0, s * L::Q_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < DK / 16; ++kk)
+            umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dKV0, kk * 2048), ID_O,
                          kk > 0);
-          }
-          umma_commit(&bars[B_PFREE]);
+          umma_commit(&bars[L::B_OFULL]);
         }
-        // dKV = K~^T V   (M = DK, K = 128 tokens)
+        __syncwarp();
+      } else {
+        mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
+      }
+      // dKV = K~^T V  (M = DK, K = 128 tokens)
+      mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
+      if (i >= 1) mbar_wait(&bars[L::B_DKVEMPTY], (i - 1) & 1);
+      TR(1, i, 5);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t kt_d = adv(dKT0, kt * L::K_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk) {
-          umma_bf16_ss(tKV(s), sdesc_sw128(sK + s * L::K_BYTES + kk * 2048, REGION, 1024),
-                       sdesc_sw128(sV + s * L::V_BYTES + kk * 2048, REGION, 1024), ID_KV,
-                       kk > 0);
+        for (int kk = 0; kk < BT / 16; ++kk)
+          umma_bf16_ss(tKV, adv(kt_d, kk * 2048), adv(v, kk * 2048), ID_KV, kk > 0);
+        umma_commit(&bars[L::B_DKVFULL]);
+        umma_commit(&bars[L::B_KTFREE + kt]);
+        umma_commit(&bars[L::B_EMPTY + s]);
+      }
+      __syncwarp();
+      TR(1, i, 6);
+    }
+  } else if (warp < W0) {
+    // --------------------------------------------------------------- row warps
+    if (!SO) {
+      const int q4 = warp & 3;             // TMEM lane quarter
+      const int half = (warp - 2) >> 2;    // column half handled by this warp
+      const int row = q4 * 32 + lane;
+      const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+      // Mask factors for this row and this warp's 4 chunks of 16 score columns:
+      //   M[row][16ch + j] = (ch == dch) ? Dg[j] : F[ch] * G[j]   (F = 0 on the zero side)
+      float G[16], Dg[16], F[4];
+      const int dch = row >> 4, tt = row & 15;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (!REV) {
+          G[j] = lam_pow(l2, 15 - j);
+          Dg[j] = (j <= tt) ? lam_pow(l2, tt - j) : 0.f;
+        } else {
+          G[j] = lam_pow(l2, j);
+          Dg[j] = (j >= tt) ? lam_pow(l2, j - tt) : 0.f;
         }
-        if (!SO) {
-          // O += Q~ KV_{i-1}   (K = DK)
-          mbar_wait(&bars[B_KVREADY], i & 1);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ch = 4 * half + c;
+        if (!REV) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
+        else F[c] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
+      }
+      for (int j = 0; j <= nblk; ++j) {
+        if (j < nblk) {
+          // ---- A(j): S -> P (bf16). This warp reads score columns [64h, 64h+64) and
+          // writes the packed P pairs into columns [64h, 64h+32) of the same buffer.
+          const int b = j & 1;
+          const uint32_t tS = tbase + b * 128 + half * 64 + lane_off;
+          if (warp == 2) TR(2, j, 0);
+          mbar_wait(&bars[L::B_SFULL + b], (j >> 1) & 1);
+          if (warp == 2) TR(2, j, 1);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < DK / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * REGION + (kk & 3) * 32;
-            umma_bf16_ss(tO(s), sdesc_sw128(sQ + s * L::Q_BYTES + off, 16, 1024),
-                         sdesc_sw128(sKV + kk * 2048, DK * 128, 1024), ID_O, 1);
+          for (int hh = 0; hh < 2; ++hh) {  // 32 score columns -> 16 packed columns
+            uint32_t raw[32];
+            tmem_ld32_raw(tS + hh * 32, raw);
+            tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int c = 2 * hh + (e >> 3), ch = 4 * half + c, jj = (2 * e) & 15;
+              const float m0 = (ch == dch) ? Dg[jj] : F[c] * G[jj];
+              const float m1 = (ch == dch) ? Dg[jj + 1] : F[c] * G[jj + 1];
+              pk[e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * m0,
+                                  __uint_as_float(raw[2 * e + 1]) * m1);
+            }
+            tmem_st16(tS + hh * 16, pk);
           }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[L::B_PREADY + b]);
+          if (warp == 2) TR(2, j, 2);
         }
-        umma_commit(&bars[B_OFULL + s]);
-        umma_commit(&bars[B_EMPTY + s]);
+        if (j >= 1) {
+          // ---- B(j-1): o = O + a_t Oe for value columns [32h, 32h+32) -> smem -> TMA store
+          const int i = j - 1;
+          const int blk = REV ? (nblk - 1 - i) : i;
+          const int r = min(BT, N - blk * BT);
+          const float a = REV ? (row < r ? lam_pow(l2, r - 1 - row) : 0.f) : lam_pow(l2, row + 1);
+          uint8_t* sO = smem + L::OFF_O + (i % OS) * L::O_BYTES;
+          const bool storer = (half == 0 && lane == 0);
+          if (warp == 2) TR(2, i, 3);
+          if (storer) tma_store_wait_read<OS - 1>();
+          named_bar_sync(1 + q4, 64);  // the two warps of this quarter
+          if (warp == 2) TR(2, i, 4);
+          mbar_wait(&bars[L::B_OFULL], i & 1);
+          if (warp == 2) TR(2, i, 5);
+          tc_fence_after();
+          float o16[2][16], e16[2][16];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            tmem_ld16(tbase + L::T_O + lane_off + half * 32 + q * 16, o16[q]);
+            tmem_ld16(tbase + L::T_OE + lane_off + half * 32 + q * 16, e16[q]);
+          }
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[L::B_OEMPTY]);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o16[q][e] = fmaf(a, e16[q][e], o16[q][e]);
+            store_chunk16_bf16(sO, row, 2 * half + q, o16[q]);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1 + q4, 64);
+          if (storer) {
+            tma_store_3d(&tm_o, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
+            tma_store_commit();
+          }
+          if (warp == 2) TR(2, i, 6);
+        }
       }
+      if (half == 0 && lane == 0) tma_store_wait_all0();
     }
   } else {
-    // --------------------------------------------------------------- row warps
-    const int q4 = warp & 3;                 // TMEM lane quarter owned by this warp
-    const int row = q4 * 32 + lane;          // token row within the block
-    const int ct = threadIdx.x - 64;         // 0..127
+    // ------------------------------------------------------------- state warps
+    const int q4 = warp & 3;  // warps 10-13 -> quarters 2,3,0,1
+    const int row = q4 * 32 + lane;  // token row for K~
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    const float lam = p.decay[h];
-    // exact log2 (fast-math log2f is off by ~2^-22 absolute, which compounds over
-    // 64K tokens when lam is close to 1)
-    const float l2 = (lam >= 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
-    // KV rows: M=128 -> lane == d row; M=64 -> lanes 0-15 of each quarter hold 16 rows.
+    // dKV rows: M=128 -> lane == d row; M=64 -> lanes 0-15 of each quarter hold 16 rows
     const bool has_kv = (DK == 128) || (lane < 16);
     const int kvrow = (DK == 128) ? row : (q4 * 16 + lane);
     const int dvt = p.dv_total;
     const size_t sbase = static_cast<size_t>(bh) * DK * dvt;
-
-    // Mask factors for this row (block-invariant): M[row][16ch + j] =
-    //   ch == dch ? Dg[j] : F[ch] * G[j]   (F = 0 for the zero side).
-    float G[16], Dg[16], F[8];
-    const int dch = row >> 4, tt = row & 15;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (!REV) {
-        G[j] = lam_pow(l2, 15 - j);
-        Dg[j] = (j <= tt) ? lam_pow(l2, tt - j) : 0.f;
-      } else {
-        G[j] = lam_pow(l2, j);
-        Dg[j] = (j >= tt) ? lam_pow(l2, j - tt) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-      if (!REV) F[ch] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
-      else F[ch] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
-    }
-
     float kv[DVS];
 #pragma unroll
     for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
@@ -314,117 +428,70 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       } else {
         // state stored transposed: [dv_total][DK]
 #pragma unroll
-        for (int j = 0; j < DVS; ++j) kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * DK + kvrow];
+        for (int j = 0; j < DVS; ++j)
+          kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * DK + kvrow];
       }
     }
     uint8_t* sKVb = smem + L::OFF_KV;
-    uint8_t* sO = smem + L::OFF_O;
     if (!SO) {
-      if (has_kv) store_row64_bf16(sKVb, kvrow, kv);
+      if (has_kv) {
+#pragma unroll
+        for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
+      }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_KVREADY]);
+      if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
     }
-
     for (int j = 0; j <= nblk; ++j) {
-      // ---------------- phase A(j): S -> P, scale Q and K rows in place
       if (j < nblk) {
-        const int i = j, s = i & 1;
-        const int blk = REV ? (nblk - 1 - i) : i;
+        // ---- K~(j): scaled copy of the K rows
+        const int s = j % NS, kt = j % KTS;
+        const int blk = REV ? (nblk - 1 - j) : j;
         const int r = min(BT, N - blk * BT);
-        const float a = REV ? (row < r ? lam_pow(l2, r - 1 - row) : 0.f) : lam_pow(l2, row + 1);
         const float c = REV ? lam_pow(l2, row + 1) : (row < r ? lam_pow(l2, r - 1 - row) : 0.f);
-        if (!SO) {
-          mbar_wait(&bars[B_SFULL + s], (i >> 1) & 1);
-          tc_fence_after();
-          scale_row_inplace<DK>(smem + L::OFF_Q + s * L::Q_BYTES, row, a);
-          scale_row_inplace<DK>(smem + L::OFF_K + s * L::K_BYTES, row, c);
-          if (i >= 1) mbar_wait(&bars[B_PFREE], (i - 1) & 1);
-          uint8_t* sP = smem + L::OFF_P;
-#pragma unroll
-          for (int cp = 0; cp < 4; ++cp) {  // pairs of 16-column chunks
-            float v0[16], v1[16];
-            tmem_ld16(tS(s) + lane_off + cp * 32, v0);
-            tmem_ld16(tS(s) + lane_off + cp * 32 + 16, v1);
-            tmem_ld_wait();
-            float x[32];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int ch0 = 2 * cp, ch1 = 2 * cp + 1;
-              const float m0 = (ch0 == dch) ? Dg[e] : F[ch0] * G[e];
-              const float m1 = (ch1 == dch) ? Dg[e] : F[ch1] * G[e];
-              x[e] = v0[e] * m0;
-              x[16 + e] = v1[e] * m1;
-            }
-            // columns 32cp .. 32cp+31 -> region cp/2, logical chunks 4*(cp&1) .. +3
-            uint8_t* rp = sP + (cp >> 1) * REGION + row * 128;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int lc = 4 * (cp & 1) + q;
-              uint4 w;
-              w.x = pack_bf16x2(x[8 * q + 0], x[8 * q + 1]);
-              w.y = pack_bf16x2(x[8 * q + 2], x[8 * q + 3]);
-              w.z = pack_bf16x2(x[8 * q + 4], x[8 * q + 5]);
-              w.w = pack_bf16x2(x[8 * q + 6], x[8 * q + 7]);
-              *reinterpret_cast<uint4*>(rp + ((lc ^ (row & 7)) * 16)) = w;
-            }
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[B_SEMPTY + s]);
-        } else {
-          mbar_wait(&bars[B_FULL + s], (i >> 1) & 1);
-          scale_row_inplace<DK>(smem + L::OFF_K + s * L::K_BYTES, row, c);
-        }
+        if (warp == W0) TR(3, j, 0);
+        mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+        if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
+        if (warp == W0) TR(3, j, 1);
+        scale_row_copy<DK>(smem + L::OFF_K + s * L::K_BYTES, smem + L::OFF_KT + kt * L::K_BYTES,
+                           row, c);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_PREADY]);
+        if (lane == 0) mbar_arrive(&bars[L::B_KTREADY + kt]);
+        if (warp == W0) TR(3, j, 2);
       }
-      // ---------------- phase B(j-1): O epilogue and KV state update
       if (j >= 1) {
-        const int i = j - 1, s = i & 1;
+        // ---- U(j-1): KV <- lam^r KV + dKV
+        const int i = j - 1;
         const int blk = REV ? (nblk - 1 - i) : i;
         const int r = min(BT, N - blk * BT);
-        mbar_wait(&bars[B_OFULL + s], (i >> 1) & 1);
-        tc_fence_after();
         const float fr = lam_pow(l2, static_cast<float>(r));
-        if (!SO) {
-          // previous O tile must have been read out of the staging buffer
-          if (ct == 0) tma_store_wait_read0();
-          named_bar_sync(1, 128);
-        }
+        if (warp == W0) TR(3, i, 3);
+        mbar_wait(&bars[L::B_DKVFULL], i & 1);
+        if (warp == W0) TR(3, i, 4);
+        tc_fence_after();
 #pragma unroll
         for (int q = 0; q < DVS / 16; ++q) {
-          float d16[16], o16[16];
-          tmem_ld16(tKV(s) + lane_off + q * 16, d16);
-          if (!SO) tmem_ld16(tO(s) + lane_off + q * 16, o16);
+          float d16[16];
+          tmem_ld16(tbase + L::T_KV + lane_off + q * 16, d16);
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) kv[16 * q + e] = fmaf(fr, kv[16 * q + e], d16[e]);
-          }
-          if (!SO) {
-            if (has_kv) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
-            store_chunk16_bf16(sO, row, q, o16);
+            if (!SO) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_OEMPTY + s]);
+        if (lane == 0) mbar_arrive(&bars[L::B_DKVEMPTY]);
         if (!SO) {
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[B_KVREADY]);
-          // O tile -> TMA store (rows >= r are clipped by the tensor map)
-          named_bar_sync(1, 128);
-          if (ct == 0) {
-            tma_store_3d(&tm_o, sO, slice * DVS, blk * BT, bh);
-            tma_store_commit();
-          }
+          if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
         }
+        if (warp == W0) TR(3, i, 5);
       }
     }
-    if (!SO && ct == 0) tma_store_wait_all0();
     if (p.kv_out != nullptr && has_kv) {
       float* dst = p.kv_out + sbase + static_cast<size_t>(kvrow) * dvt + slice * DVS;
 #pragma unroll
@@ -452,12 +519,12 @@ static int get_encode() {
 }
 
 // [BH][N][cols] bf16, box (64 cols, 128 rows, 1 head), 128B swizzle.
-static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH) {
+static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
                         static_cast<cuuint64_t>(BH)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2,
                            static_cast<cuuint64_t>(cols) * 2 * static_cast<cuuint64_t>(N)};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(BT), 1};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -479,7 +546,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st) {
   const int cols[4] = {DK, DK, a.dv, a.dv};
   for (int t = 0; t < 4; ++t) {
     if (SO && (t == 0 || t == 3)) continue;
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH);
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, t == 3 ? 32 : BT);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),
@@ -503,6 +570,13 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   return 0;
 }
+
+#ifdef LA2_TRACE
+extern "C" LA2_API int la2_set_trace(long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
+  return e == cudaSuccess ? 0 : set_cuda_error("la2_set_trace", e);
+}
+#endif
 
 int launch_tc(const FArgs& a, cudaStream_t st) {
   if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");

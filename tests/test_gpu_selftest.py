@@ -11,7 +11,12 @@ from paper_2401_04658_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("M,N,K,a_mn,b_mn", list(itertools.product((64, 128), (64, 128), (64, 128), (0, 1), (0, 1))))
+CASES = list(itertools.product((64, 128), (64, 128), (64, 128), (0, 1), (0, 1)))
+# a_mn == 2: A operand read from TMEM (tcgen05.mma ... [a_tmem]), M = 128 only
+CASES += list(itertools.product((128,), (64, 128), (64, 128), (2,), (0, 1)))
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", CASES)
 def test_umma_layouts(M, N, K, a_mn, b_mn):
     g = torch.Generator().manual_seed(M * 7 + N * 3 + K + 2 * a_mn + b_mn)
     A = (torch.rand(M, K, generator=g) * 2 - 1).bfloat16().float()
