@@ -61,16 +61,17 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def load_traffic():
-    """dram bytes per launch of the forward F kernel from the committed ncu summary."""
+def load_traffic(tokens_heads: int):
+    """DRAM bytes of one forward F launch, from the committed ncu --set full capture
+    (profiles/ncu_summary.json: dram read+write per token-head), scaled to B*H*N."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
             j = json.loads(p.read_text())
-            return j.get("fwd_dram_bytes_per_launch"), j
+            return j["fwd_dram_bytes_per_token_head"] * tokens_heads
         except Exception:
             pass
-    return None, None
+    return None
 
 
 class ClockSampler:
@@ -269,7 +270,7 @@ def main():
     ms_bwd = time_steps(lambda: la2.la2_backward(q, k, v, do, decay), max(3, args.steps), 2)
     fwd_bytes = bf * B * H
     achieved = fwd_bytes / (ms_fwd / 1e3) / 1e9
-    traffic, _ = load_traffic()
+    traffic = load_traffic(B * H * N)
     roofline = {"bound": "hbm", "kernel": "la2_tc_kernel<64,fwd> (one F launch = the forward pass)",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": fwd_bytes,
