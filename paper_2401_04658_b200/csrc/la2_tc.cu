@@ -19,9 +19,11 @@
 //   KV_i   = lam^r KV_{i-1} + dKV                   fp32 registers of the state warps
 // The fp32 KV state never leaves the SM.
 //
-// Warp roles (448 threads, one CTA per SM):
+// Warp roles (480 threads, one CTA per SM):
 //   warp 0     TMA producer (Q/K/V ring of NS stages)
-//   warp 1     MMA issuer (one thread) + TMEM owner
+//   warp 1     MMA issuer X (S = QK^T, O = PV) + TMEM owner
+//   warp 14    MMA issuer Y (dKV = K~^T V, Oe = Q KV): the state chain never waits
+//              behind the score chain, so a late load cannot stall the recurrence
 //   warps 2-9  row warps:   thread <-> token row, two warps per TMEM lane quarter
 //              splitting the columns; S -> P, O epilogue + TMA store
 //   warps 10-13 state warps: K~ rows, dKV -> fp32 KV state -> bf16 KV operand
@@ -53,9 +55,10 @@ constexpr int TR_MAXB = 64, TR_EV = 8;
 
 constexpr int BT = 128;        // tokens per block
 constexpr int DVS = 64;        // value columns per CTA (dv slice)
-constexpr int TC_THREADS = 448;  // 14 warps
+constexpr int TC_THREADS = 480;  // 15 warps
 constexpr int NROW = 8;         // row warps (2 per TMEM lane quarter)
-constexpr int W0 = 2 + NROW;    // first state warp
+constexpr int W0 = 2 + NROW;    // first state warp (4 state warps)
+constexpr int WY = W0 + 4;      // second MMA issuer (state chain)
 constexpr int REGION = BT * 64 * 2;  // one [128][64] bf16 SW128 region = 16 KB
 
 template <int DK, bool SO>
@@ -78,15 +81,16 @@ struct TcLayout {
   static constexpr int BAR_BYTES = 256;
   static constexpr int TOTAL = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
-  // TMEM columns: S[2] @0,128 (P aliased) | O @256 | Oe @320 | dKV @384 (state-only: dKV @0)
+  // TMEM columns: S[2] @0,128 (P aliased) | O @256 | Oe @320 | dKV[2] @384,448
+  // (state-only: dKV[2] @0,64)
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
   static constexpr uint32_t T_O = 256, T_OE = 320, T_KV = SO ? 0 : 384;
   // barrier slots
   static constexpr int B_FULL = 0, B_EMPTY = NS, B_SFULL = 2 * NS, B_SFREE = B_SFULL + 2,
-                       B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEMPTY = B_OFULL + 1,
-                       B_KTREADY = B_OEMPTY + 1, B_KTFREE = B_KTREADY + KTS,
-                       B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 1,
-                       B_KVREADY = B_DKVEMPTY + 1, B_COUNT = B_KVREADY + 1;
+                       B_PREADY = B_SFREE + 2, B_OFULLX = B_PREADY + 2, B_OEFULL = B_OFULLX + 1,
+                       B_OEMPTY = B_OEFULL + 1, B_KTREADY = B_OEMPTY + 1, B_KTFREE = B_KTREADY + KTS,
+                       B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 2,
+                       B_KVREADY = B_DKVEMPTY + 2, B_COUNT = B_KVREADY + 1;
   static_assert(B_COUNT * 8 + 16 <= BAR_BYTES, "barrier area");
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
@@ -98,17 +102,19 @@ __device__ __forceinline__ void scale_row_copy(const uint8_t* src, uint8_t* dst,
   for (int reg = 0; reg < DK / 64; ++reg) {
     const uint8_t* sp = src + reg * REGION + row * 128;
     uint8_t* dp = dst + reg * REGION + row * 128;
+    uint4 w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = *reinterpret_cast<const uint4*>(sp + ((k + row) & 7) * 16);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = (k + row) & 7;  // rotate chunks to spread banks across the warp
-      uint4 w = *reinterpret_cast<const uint4*>(sp + c * 16);
-      uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+      uint32_t* u = reinterpret_cast<uint32_t*>(&w[k]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float2 x = unpack_bf16x2(u[e]);
         u[e] = pack_bf16x2(x.x * f, x.y * f);
       }
-      *reinterpret_cast<uint4*>(dp + c * 16) = w;
+      // chunks are rotated by row to spread banks across the warp
+      *reinterpret_cast<uint4*>(dp + ((k + row) & 7) * 16) = w[k];
     }
   }
 }
@@ -156,21 +162,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[L::B_FULL + s], 1);
-      mbar_init(&bars[L::B_EMPTY + s], 1);
+      mbar_init(&bars[L::B_EMPTY + s], SO ? 1 : 2);  // X after PV, Y after Oe
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[L::B_SFULL + b], 1);
       mbar_init(&bars[L::B_SFREE + b], 1);
       mbar_init(&bars[L::B_PREADY + b], NROW);
     }
-    mbar_init(&bars[L::B_OFULL], 1);
+    mbar_init(&bars[L::B_OFULLX], 1);
+    mbar_init(&bars[L::B_OEFULL], 1);
     mbar_init(&bars[L::B_OEMPTY], NROW);
     for (int b = 0; b < KTS; ++b) {
       mbar_init(&bars[L::B_KTREADY + b], 4);
       mbar_init(&bars[L::B_KTFREE + b], 1);
     }
-    mbar_init(&bars[L::B_DKVFULL], 1);
-    mbar_init(&bars[L::B_DKVEMPTY], 4);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[L::B_DKVFULL + b], 1);
+      mbar_init(&bars[L::B_DKVEMPTY + b], 4);
+    }
     mbar_init(&bars[L::B_KVREADY], 4);
     fence_barrier_init();
   }
@@ -214,8 +223,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     row, bh);
       }
     }
-  } else if (warp == 1) {
-    // -------------------------------------------------------------- MMA issuer
+  } else if (warp == 1 || warp == WY) {
+    // ------------------------------------------------------------- MMA issuers
     // The whole warp walks the schedule (converged barrier waits); one lane issues.
     constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K (K-major)
     constexpr uint32_t ID_O = idesc_bf16(128, DVS, 0, 1);  // P/Q (K-major) x V/KV (MN-major)
@@ -230,77 +239,87 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint64_t dKV0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), DK * 128, 1024);
     auto adv = [](uint64_t d, uint32_t bytes) { return d + static_cast<uint64_t>(bytes >> 4); };
 
-    auto issue_S = [&](int j) {
-      const int s = j % NS, b = j & 1;
-      mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
-      if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
-      tc_fence_after();
-      if (leader) {
-        const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < DK / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * REGION + (kk & 3) * 32;
-          umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
-        }
-        umma_commit(&bars[L::B_SFULL + b]);
-      }
-      __syncwarp();
-    };
-
-    if (!SO) issue_S(0);
-    for (int i = 0; i < nblk; ++i) {
-      const int s = i % NS, b = i & 1, kt = i % KTS;
-      const uint64_t v = adv(dV0, s * L::V_BYTES);
+    if (warp == 1) {
+      // ---- X: score chain  S_{i+1} = Q K^T ; O_i = P_i V_i
       if (!SO) {
-        TR(1, i, 0);
-        if (i + 1 < nblk) issue_S(i + 1);
-        TR(1, i, 1);
-        // O = P V  (A = P in TMEM over S[b], K = 128 tokens)
-        mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
-        TR(1, i, 2);
-        if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
-        TR(1, i, 3);
+        auto issue_S = [&](int j) {
+          const int s = j % NS, b = j & 1;
+          mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+          if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
+          tc_fence_after();
+          if (leader) {
+            const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < DK / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * REGION + (kk & 3) * 32;
+              umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
+            }
+            umma_commit(&bars[L::B_SFULL + b]);
+          }
+          __syncwarp();
+        };
+        issue_S(0);
+        for (int i = 0; i < nblk; ++i) {
+          const int s = i % NS, b = i & 1;
+          const uint64_t v = adv(dV0, s * L::V_BYTES);
+          TR(1, i, 0);
+          if (i + 1 < nblk) issue_S(i + 1);
+          TR(1, i, 1);
+          mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
+          TR(1, i, 2);
+          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
+          TR(1, i, 3);
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < BT / 16; ++kk)
+              umma_bf16_ts(tO, tbase + b * 128 + (kk >> 2) * 64 + (kk & 3) * 8, adv(v, kk * 2048),
+                           ID_O, kk > 0);
+            umma_commit(&bars[L::B_SFREE + b]);
+            umma_commit(&bars[L::B_OFULLX]);
+            umma_commit(&bars[L::B_EMPTY + s]);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      // ---- Y: state chain  dKV_i = K~_i^T V_i (early) ; Oe_i = Q_i KV_{i-1}
+      for (int i = 0; i < nblk; ++i) {
+        const int s = i % NS, kt = i % KTS, db = i & 1;
+        const uint64_t v = adv(dV0, s * L::V_BYTES);
+        mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
+        if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
+        mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
+        TR(1, i, 5);
         tc_fence_after();
         if (leader) {
+          const uint64_t kt_d = adv(dKT0, kt * L::K_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
-            umma_bf16_ts(tO, tbase + b * 128 + (kk >> 2) * 64 + (kk & 3) * 8, adv(v, kk * 2048),
-                         ID_O, kk > 0);
-          umma_commit(&bars[L::B_SFREE + b]);
+            umma_bf16_ss(tKV + db * 64, adv(kt_d, kk * 2048), adv(v, kk * 2048), ID_KV, kk > 0);
+          umma_commit(&bars[L::B_DKVFULL + db]);
+          umma_commit(&bars[L::B_KTFREE + kt]);
+          if (SO) umma_commit(&bars[L::B_EMPTY + s]);
         }
         __syncwarp();
-        // Oe = Q KV_{i-1}  (K = DK)
-        mbar_wait(&bars[L::B_KVREADY], i & 1);
-        TR(1, i, 4);
-        tc_fence_after();
-        if (leader) {
-          const uint64_t q = adv(dQ0, s * L::Q_BYTES);
+        if (!SO) {
+          mbar_wait(&bars[L::B_KVREADY], i & 1);
+          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
+          TR(1, i, 4);
+          tc_fence_after();
+          if (leader) {
+            const uint64_t q = adv(dQ0, s * L::Q_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < DK / 16; ++kk)
-            umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dKV0, kk * 2048), ID_O,
-                         kk > 0);
-          umma_commit(&bars[L::B_OFULL]);
+            for (int kk = 0; kk < DK / 16; ++kk)
+              umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dKV0, kk * 2048),
+                           ID_O, kk > 0);
+            umma_commit(&bars[L::B_OEFULL]);
+            umma_commit(&bars[L::B_EMPTY + s]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-      } else {
-        mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
+        TR(1, i, 6);
       }
-      // dKV = K~^T V  (M = DK, K = 128 tokens)
-      mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
-      if (i >= 1) mbar_wait(&bars[L::B_DKVEMPTY], (i - 1) & 1);
-      TR(1, i, 5);
-      tc_fence_after();
-      if (leader) {
-        const uint64_t kt_d = adv(dKT0, kt * L::K_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          umma_bf16_ss(tKV, adv(kt_d, kk * 2048), adv(v, kk * 2048), ID_KV, kk > 0);
-        umma_commit(&bars[L::B_DKVFULL]);
-        umma_commit(&bars[L::B_KTFREE + kt]);
-        umma_commit(&bars[L::B_EMPTY + s]);
-      }
-      __syncwarp();
-      TR(1, i, 6);
     }
   } else if (warp < W0) {
     // --------------------------------------------------------------- row warps
@@ -373,7 +392,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (storer) tma_store_wait_read<OS - 1>();
           named_bar_sync(1 + q4, 64);  // the two warps of this quarter
           if (warp == 2) TR(2, i, 4);
-          mbar_wait(&bars[L::B_OFULL], i & 1);
+          mbar_wait(&bars[L::B_OFULLX], i & 1);
+          mbar_wait(&bars[L::B_OEFULL], i & 1);
           if (warp == 2) TR(2, i, 5);
           tc_fence_after();
           float o16[2][16], e16[2][16];
@@ -403,7 +423,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (half == 0 && lane == 0) tma_store_wait_all0();
     }
-  } else {
+  } else if (warp < WY) {
     // ------------------------------------------------------------- state warps
     const int q4 = warp & 3;  // warps 10-13 -> quarters 2,3,0,1
     const int row = q4 * 32 + lane;  // token row for K~
@@ -467,24 +487,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int r = min(BT, N - blk * BT);
         const float fr = lam_pow(l2, static_cast<float>(r));
         if (warp == W0) TR(3, i, 3);
-        mbar_wait(&bars[L::B_DKVFULL], i & 1);
+        const int db = i & 1;
+        mbar_wait(&bars[L::B_DKVFULL + db], (i >> 1) & 1);
         if (warp == W0) TR(3, i, 4);
         tc_fence_after();
 #pragma unroll
         for (int q = 0; q < DVS / 16; ++q) {
           float d16[16];
-          tmem_ld16(tbase + L::T_KV + lane_off + q * 16, d16);
+          tmem_ld16(tbase + L::T_KV + db * 64 + lane_off + q * 16, d16);
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) kv[16 * q + e] = fmaf(fr, kv[16 * q + e], d16[e]);
-            if (!SO) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[L::B_DKVEMPTY]);
+        if (lane == 0) mbar_arrive(&bars[L::B_DKVEMPTY + db]);
         if (!SO) {
+          // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
+          mbar_wait(&bars[L::B_OEFULL], i & 1);
+          if (has_kv) {
+#pragma unroll
+            for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);

@@ -8,7 +8,9 @@ from paper_2401_04658_b200 import _lib
 from bench import alibi_decay
 lib = _lib.load()
 lib.la2_set_trace.argtypes = [ctypes.c_void_p]
-B, H, N, D = 8, 16, int(sys.argv[1]) if len(sys.argv) > 1 else 16384, 64
+B, H = 8, 16
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+D = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 dev = torch.device('cuda', 0)
 q, k, v = ((torch.rand(B, H, N, D, device=dev) * 2 - 1).bfloat16() for _ in range(3))
 dec = la2.decay_tensor(alibi_decay(H), H, dev)
@@ -27,4 +29,4 @@ for role in range(4):
     for i in list(range(0, 4)) + list(range(40, 46)):
         print(f"  blk {i:3d}: " + " ".join(f"{x:8d}" for x in t[role, i] if x >= 0))
 per = np.diff(t[2, 30:60, 0]).mean()
-print("steady-state cycles per block (row A start):", per)
+print("steady-state cycles per block (row A start):", per, "D =", D)
