@@ -14,8 +14,8 @@
 //   O_i    = P V_i                                  TS-MMA  (A = P from TMEM)
 //   Oe_i   = Q_i KV_{i-1}                           SS-MMA  (KV as bf16 B operand)
 //   o_t    = O_i[t] + a_t Oe_i[t]    a_t = lam^(t+1) | rev: lam^(r-1-t)   (registers)
-//   K~     = bf16(c_t K_i)           c_t = lam^(r-1-t)| rev: lam^(t+1)    (state warps)
-//   dKV    = K~^T V_i                               SS-MMA  -> TMEM
+//   V~     = bf16(c_t V_i)           c_t = lam^(r-1-t)| rev: lam^(t+1)    (state warps)
+//   dKV    = K_i^T V~                               SS-MMA  -> TMEM
 //   KV_i   = lam^r KV_{i-1} + dKV                   fp32 registers of the state warps
 // The fp32 KV state never leaves the SM.
 //
@@ -26,7 +26,7 @@
 //              behind the score chain, so a late load cannot stall the recurrence
 //   warps 2-9  row warps:   thread <-> token row, two warps per TMEM lane quarter
 //              splitting the columns; S -> P, O epilogue + TMA store
-//   warps 10-13 state warps: K~ rows, dKV -> fp32 KV state -> bf16 KV operand
+//   warps 10-13 state warps: V~ rows, dKV -> fp32 KV state -> bf16 KV operand
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -64,7 +64,7 @@ constexpr int REGION = BT * 64 * 2;  // one [128][64] bf16 SW128 region = 16 KB
 template <int DK, bool SO>
 struct TcLayout {
   static constexpr int NS = (DK == 64) ? 3 : 2;   // Q/K/V stages
-  static constexpr int KTS = (DK == 64) ? 2 : 1;  // K~ buffers
+  static constexpr int KTS = 2;                   // V~ buffers (scaled values)
   static constexpr int OS = (DK == 64 && !SO) ? 2 : 1;  // O staging buffers
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
   static constexpr int K_BYTES = BT * DK * 2;
@@ -75,7 +75,7 @@ struct TcLayout {
   static constexpr int OFF_K = OFF_Q + NS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
   static constexpr int OFF_KT = OFF_V + NS * V_BYTES;
-  static constexpr int OFF_KV = OFF_KT + KTS * K_BYTES;
+  static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
   static constexpr int OFF_O = OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
   static constexpr int BAR_BYTES = 256;
@@ -203,7 +203,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      // With a 2-stage ring (d = 128: 80 KB stages) a stage is refilled only one block
+      // ahead, which exposes HBM latency; pull the next PF blocks into L2 so the ring's
+      // TMA loads hit L2.
+      constexpr int PF = (NS == 2) ? 3 : 0;
+      auto prefetch = [&](int i) {
+        const int b2 = REV ? (nblk - 1 - i) : i;
+#pragma unroll
+        for (int c = 0; c < DK / 64; ++c) {
+          if (!SO) tma_prefetch_l2_3d(&tm_q, c * 64, b2 * BT, bh);
+          tma_prefetch_l2_3d(&tm_k, c * 64, b2 * BT, bh);
+        }
+        tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
+      };
+      for (int i = NS; i < NS + PF && i < nblk; ++i) prefetch(i);
       for (int i = 0; i < nblk; ++i) {
+        if (PF > 0 && i + NS + PF < nblk) prefetch(i + NS + PF);
         const int blk = REV ? (nblk - 1 - i) : i;
         const int s = i % NS;
         TR(0, i, 0);
@@ -293,10 +308,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         TR(1, i, 5);
         tc_fence_after();
         if (leader) {
-          const uint64_t kt_d = adv(dKT0, kt * L::K_BYTES);
+          // dKV = K^T (c . V): A = K^T (MN-major view of the K stage), B = V~ (MN-major)
+          const uint64_t vt_d = adv(dKT0, kt * L::V_BYTES);
+          const uint64_t kA = sdesc_sw128(smem_u32(smem + L::OFF_K + s * L::K_BYTES), REGION, 1024);
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
-            umma_bf16_ss(tKV + db * 64, adv(kt_d, kk * 2048), adv(v, kk * 2048), ID_KV, kk > 0);
+            umma_bf16_ss(tKV + db * 64, adv(kA, kk * 2048), adv(vt_d, kk * 2048), ID_KV, kk > 0);
           umma_commit(&bars[L::B_DKVFULL + db]);
           umma_commit(&bars[L::B_KTFREE + kt]);
           if (SO) umma_commit(&bars[L::B_EMPTY + s]);
@@ -473,7 +490,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
         if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
         if (warp == W0) TR(3, j, 1);
-        scale_row_copy<DK>(smem + L::OFF_K + s * L::K_BYTES, smem + L::OFF_KT + kt * L::K_BYTES,
+        scale_row_copy<64>(smem + L::OFF_V + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
                            row, c);
         fence_proxy_async_smem();
         __syncwarp();
