@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libla2.so"
-SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_simt.cu", "la2_selftest.cu"]
+SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_bwd.cu", "la2_simt.cu", "la2_selftest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

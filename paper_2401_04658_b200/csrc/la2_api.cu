@@ -2,6 +2,7 @@
 // error semantics (pkg/src/tila/reference.py:42-74, kernel.py:68-70), kernel
 // selection, and the backward pass expressed as three F passes.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "la2_kernels.h"
@@ -35,11 +36,11 @@ static int check_common(int B, int H, int N, int d, int dv, int dtype, const flo
   if (dtype != LA2_BF16 && dtype != LA2_FP32)
     return set_error(LA2_ERR_UNSUPPORTED, "dtype must be LA2_BF16 or LA2_FP32");
   if (decay == nullptr) return set_error(LA2_ERR_VALUE, "decay pointer is null");
-  if (!tc_eligible(dtype, d, dv) && (d > 128 || dv > 128)) {
+  if (!tc_eligible(dtype, d, dv) && (d > 256 || dv > 256)) {
     char buf[160];
     std::snprintf(buf, sizeof(buf),
                   "unsupported shape d=%d dv=%d for dtype %s (bf16 tensor-core path: d in "
-                  "{64,128}, dv %% 64 == 0; otherwise d, dv <= 128)",
+                  "{64,128}, dv %% 64 == 0; otherwise d, dv <= 256)",
                   d, dv, dtype == LA2_BF16 ? "bf16" : "fp32");
     return set_error(LA2_ERR_UNSUPPORTED, buf);
   }
@@ -106,6 +107,10 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
   // dQ = F(dO, V, K): forward scan, state KV^T  (tiled_backward sweep 1, kernel.py:184-204)
   FArgs aq{dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, dtype, 0};
   if (int rc = run_f(aq, st)) return rc;
+  // d = dv = 64 bf16: dK and dV in one fused reverse scan (sweep 2, kernel.py:207-231)
+  static const bool no_fused = std::getenv("LA2_NO_FUSED_BWD") != nullptr;
+  if (dtype == LA2_BF16 && d == 64 && dvd == 64 && !no_fused)
+    return launch_g(q, k, v, dout, dk, dv, decay, dkv_in, dkv_out, B, H, N, st);
   // dK = F_rev(V, dO, Q): reverse scan, state dKV^T  (sweep 2, kernel.py:207-216)
   FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
   if (int rc = run_f(ak, st)) return rc;

@@ -1,5 +1,6 @@
 // Internal launcher interface shared by the kernel translation units and the C ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/la2.h"
@@ -35,6 +36,13 @@ struct FParams {
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);
+// Fused reverse scan of the backward pass (dK and dV together), d = dv = 64, bf16.
+int launch_g(const void* q, const void* k, const void* v, const void* dout, void* dk, void* dv,
+             const float* decay, const float* dkv_in, float* dkv_out, int B, int H, int N,
+             cudaStream_t st);
+// TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle.
+int tma_encoder_ready();
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows);
 int launch_simt(const FArgs& a, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);

@@ -33,12 +33,15 @@ __device__ __forceinline__ void st_el<__nv_bfloat16>(__nv_bfloat16* p, float x) 
 }
 
 // Same recurrence and conventions as la2_tc_kernel (see la2_tc.cu), block size 32.
+// One CTA per (b, h, value slice of width <= 64): the state slice is dk x dvs.
 template <typename T, bool REV>
 __global__ void __launch_bounds__(SIMT_THREADS)
     la2_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
-                    T* __restrict__ o, FParams p, int dk) {
+                    T* __restrict__ o, FParams p, int dk, int dvs_max) {
   extern __shared__ float sm[];
-  const int dv = p.dv_total;
+  const int dvt = p.dv_total;
+  const int c0 = blockIdx.x * dvs_max;              // first value column of this slice
+  const int dv = min(dvs_max, dvt - c0);            // slice width
   const int h = blockIdx.y;
   const int bh = blockIdx.z * p.H + h;
   const int N = p.N;
@@ -63,17 +66,18 @@ __global__ void __launch_bounds__(SIMT_THREADS)
       if (acc < 1.17549435e-38f) flushed = true;
     }
   }
-  const size_t sbase = static_cast<size_t>(bh) * dk * dv;
+  const size_t sbase = static_cast<size_t>(bh) * dk * dvt;
   for (int e = tid; e < dk * dv; e += SIMT_THREADS) {
     float x = 0.f;
     if (p.kv_in != nullptr) {
       const int c = e / dv, j = e % dv;
-      x = p.kv_in_T ? p.kv_in[sbase + static_cast<size_t>(j) * dk + c] : p.kv_in[sbase + e];
+      x = p.kv_in_T ? p.kv_in[sbase + static_cast<size_t>(c0 + j) * dk + c]
+                    : p.kv_in[sbase + static_cast<size_t>(c) * dvt + c0 + j];
     }
     KV[e] = x;
   }
   const size_t qbase = static_cast<size_t>(bh) * N * dk;
-  const size_t vbase = static_cast<size_t>(bh) * N * dv;
+  const size_t vbase = static_cast<size_t>(bh) * N * dvt + c0;
   const int nblk = (N + SB - 1) / SB;
   __syncthreads();
 
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(SIMT_THREADS)
     }
     for (int e = tid; e < SB * dv; e += SIMT_THREADS) {
       const int t = e / dv, j = e % dv;
-      Vs[t * ldv + j] = (t < r) ? ld_el<T>(v + vbase + static_cast<size_t>(t0 + t) * dv + j) : 0.f;
+      Vs[t * ldv + j] = (t < r) ? ld_el<T>(v + vbase + static_cast<size_t>(t0 + t) * dvt + j) : 0.f;
     }
     __syncthreads();
     if (!so) {
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(SIMT_THREADS)
         float inter = 0.f;
         for (int c = 0; c < dk; ++c) inter = fmaf(Qs[t * ldq + c], KV[c * dv + j], inter);
         const float a = REV ? pw[r - 1 - t] : pw[t + 1];
-        st_el<T>(o + vbase + static_cast<size_t>(t0 + t) * dv + j, intra + a * inter);
+        st_el<T>(o + vbase + static_cast<size_t>(t0 + t) * dvt + j, intra + a * inter);
       }
       __syncthreads();
     }
@@ -131,12 +135,16 @@ __global__ void __launch_bounds__(SIMT_THREADS)
     __syncthreads();
   }
   if (p.kv_out != nullptr)
-    for (int e = tid; e < dk * dv; e += SIMT_THREADS) p.kv_out[sbase + e] = KV[e];
+    for (int e = tid; e < dk * dv; e += SIMT_THREADS)
+      p.kv_out[sbase + static_cast<size_t>(e / dv) * dvt + c0 + e % dv] = KV[e];
 }
 
 int launch_simt(const FArgs& a, cudaStream_t st) {
-  if (a.dk > 128 || a.dv > 128)
-    return set_error(LA2_ERR_UNSUPPORTED, "SIMT path supports d <= 128 and dv <= 128");
+  if (a.dk > 256 || a.dv > 256)
+    return set_error(LA2_ERR_UNSUPPORTED, "SIMT path supports d <= 256 and dv <= 256");
+  // value slices of <= 64 columns keep the dk x dvs fp32 state in shared memory
+  const int dvs = a.dv <= 64 ? a.dv : 64;
+  const int nslices = (a.dv + dvs - 1) / dvs;
   FParams p;
   p.N = a.N;
   p.H = a.H;
@@ -145,9 +153,9 @@ int launch_simt(const FArgs& a, cudaStream_t st) {
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
-  const size_t smem = sizeof(float) * (static_cast<size_t>(a.dk) * a.dv + 2 * SB * (a.dk + 1) +
-                                       SB * (a.dv + 1) + SB * (SB + 1) + SB + 1);
-  dim3 grid(1, a.H, a.B);
+  const size_t smem = sizeof(float) * (static_cast<size_t>(a.dk) * dvs + 2 * SB * (a.dk + 1) +
+                                       SB * (dvs + 1) + SB * (SB + 1) + SB + 1);
+  dim3 grid(nslices, a.H, a.B);
   cudaError_t e;
 #define LA2_SIMT_LAUNCH(TY, RV)                                                                   \
   do {                                                                                            \
@@ -157,7 +165,7 @@ int launch_simt(const FArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(simt)", e);                 \
     kern<<<grid, SIMT_THREADS, smem, st>>>(static_cast<const TY*>(a.q), static_cast<const TY*>(a.k), \
                                            static_cast<const TY*>(a.v), static_cast<TY*>(a.o), p, \
-                                           a.dk);                                                 \
+                                           a.dk, dvs);                                            \
   } while (0)
   if (a.dtype == LA2_FP32) {
     if (a.reverse) LA2_SIMT_LAUNCH(float, true);

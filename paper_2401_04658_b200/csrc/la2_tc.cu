@@ -31,35 +31,14 @@
 
 #include <cstdio>
 
-#include "la2_kernels.h"
-#include "la2_ptx.cuh"
+#include "la2_tc_common.cuh"
 
 namespace la2 {
 
-// Optional phase trace (build with -DLA2_TRACE): CTA (0,0,0) records clock64()
-// stamps per role / block / event into g_trace[role][block][event].
-#ifdef LA2_TRACE
-__device__ long long* g_trace = nullptr;
-constexpr int TR_MAXB = 64, TR_EV = 8;
-#define TR(role, blk, ev)                                                                        \
-  do {                                                                                           \
-    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (blk) < TR_MAXB &&  \
-        (threadIdx.x & 31) == 0)                                                                 \
-      g_trace[((role) * TR_MAXB + (blk)) * TR_EV + (ev)] = clock64();                            \
-  } while (0)
-#else
-#define TR(role, blk, ev) \
-  do {                    \
-  } while (0)
-#endif
-
-constexpr int BT = 128;        // tokens per block
-constexpr int DVS = 64;        // value columns per CTA (dv slice)
 constexpr int TC_THREADS = 480;  // 15 warps
 constexpr int NROW = 8;         // row warps (2 per TMEM lane quarter)
 constexpr int W0 = 2 + NROW;    // first state warp (4 state warps)
 constexpr int WY = W0 + 4;      // second MMA issuer (state chain)
-constexpr int REGION = BT * 64 * 2;  // one [128][64] bf16 SW128 region = 16 KB
 
 template <int DK, bool SO>
 struct TcLayout {
@@ -94,50 +73,6 @@ struct TcLayout {
   static_assert(B_COUNT * 8 + 16 <= BAR_BYTES, "barrier area");
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
-
-// Copy one token row of a K-major SW128 tile, scaled by f, into the same row of dst.
-template <int DK>
-__device__ __forceinline__ void scale_row_copy(const uint8_t* src, uint8_t* dst, int row, float f) {
-#pragma unroll
-  for (int reg = 0; reg < DK / 64; ++reg) {
-    const uint8_t* sp = src + reg * REGION + row * 128;
-    uint8_t* dp = dst + reg * REGION + row * 128;
-    uint4 w[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = *reinterpret_cast<const uint4*>(sp + ((k + row) & 7) * 16);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t* u = reinterpret_cast<uint32_t*>(&w[k]);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 x = unpack_bf16x2(u[e]);
-        u[e] = pack_bf16x2(x.x * f, x.y * f);
-      }
-      // chunks are rotated by row to spread banks across the warp
-      *reinterpret_cast<uint4*>(dp + ((k + row) & 7) * 16) = w[k];
-    }
-  }
-}
-
-// Write 16 fp32 values as bf16 into logical chunks 2q, 2q+1 of one SW128 row.
-__device__ __forceinline__ void store_chunk16_bf16(uint8_t* region, int row, int q, const float* x) {
-  uint8_t* rp = region + row * 128;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = 2 * q + h;
-    uint4 w;
-    w.x = pack_bf16x2(x[8 * h + 0], x[8 * h + 1]);
-    w.y = pack_bf16x2(x[8 * h + 2], x[8 * h + 3]);
-    w.z = pack_bf16x2(x[8 * h + 4], x[8 * h + 5]);
-    w.w = pack_bf16x2(x[8 * h + 6], x[8 * h + 7]);
-    *reinterpret_cast<uint4*>(rp + ((c ^ (row & 7)) * 16)) = w;
-  }
-}
-
-template <int N>
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
 
 template <int DK, bool REV, bool SO>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -562,7 +497,12 @@ static int get_encode() {
 }
 
 // [BH][N][cols] bf16, box (64 cols, 128 rows, 1 head), 128B swizzle.
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows);
+int tma_encoder_ready() { return get_encode(); }
 static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT) {
+  return make_tmap_bf16(m, ptr, cols, N, BH, box_rows);
+}
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
                         static_cast<cuuint64_t>(BH)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2,
@@ -615,9 +555,11 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st) {
 }
 
 #ifdef LA2_TRACE
+int set_trace_bwd(long long* buf);
 extern "C" LA2_API int la2_set_trace(long long* buf) {
   cudaError_t e = cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
-  return e == cudaSuccess ? 0 : set_cuda_error("la2_set_trace", e);
+  if (e != cudaSuccess) return set_cuda_error("la2_set_trace", e);
+  return set_trace_bwd(buf);
 }
 #endif
 

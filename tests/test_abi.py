@@ -61,8 +61,8 @@ def test_validation_errors_without_device(lib):
     # unsupported dtype
     rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 64, 64, 7, None)
     assert rc == _lib.LA2_ERR_UNSUPPORTED
-    # fp32 with d > 128 is outside both kernels' envelope (no fallback)
-    rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 256, 64, 1, None)
+    # fp32 with d > 256 is outside both kernels' envelope (no fallback)
+    rc = lib.la2_forward(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 320, 64, 1, None)
     assert rc == _lib.LA2_ERR_UNSUPPORTED
     assert b"unsupported shape" in lib.la2_last_error()
     rc = lib.la2_backward(dummy, dummy, dummy, dummy, dummy, dummy, dummy, None, None, None, None,

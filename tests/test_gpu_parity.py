@@ -109,7 +109,21 @@ def test_tc_forward_dv256():
     assert max(rel(o, ro), rel(kv, rkv)) <= BF16_TOL
 
 
-@pytest.mark.parametrize("d,dv", [(4, 7), (32, 35), (64, 64), (100, 20)])
+@pytest.mark.parametrize("dtype,tol", [(torch.bfloat16, BF16_TOL), (torch.float32, FP32_TOL)])
+def test_head_dim_256(dtype, tol):
+    """Split-d variant (north star item 3): d = 256 runs as 64-wide value slices with
+    a 256 x 64 state slice per CTA."""
+    q, k, v, do = inputs(1, 2, 300, 256, 256, dtype, seed=256)
+    decay = [0.97, 1.0]
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, output_final_state=True)
+    dq, dk, dv_, _ = la2.la2_backward(*gpu(q, k, v, do), decay)
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay)
+    rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay)
+    errs = {"o": rel(o, ro), "kv": rel(kv, rkv), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv)}
+    assert max(errs.values()) <= tol, errs
+
+
+@pytest.mark.parametrize("d,dv", [(4, 7), (32, 35), (64, 64), (100, 20), (96, 200)])
 def test_simt_fp32_shapes(d, dv):
     q, k, v, do = inputs(1, 3, 333, d, dv, torch.float32, seed=d)
     decay = [0.5, 0.97, 1.0]
@@ -320,7 +334,7 @@ def test_long_sequence_bf16():
 
 
 def test_unsupported_shapes_raise():
-    q = torch.zeros(1, 1, 8, 256, device=DEV, dtype=torch.float32)
+    q = torch.zeros(1, 1, 8, 320, device=DEV, dtype=torch.float32)
     with pytest.raises(ValueError):
         la2.la2_forward(q, q, q, 0.9)
     q = torch.zeros(1, 1, 8, 64, device=DEV, dtype=torch.float16)
