@@ -108,9 +108,16 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
   FArgs aq{dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, dtype, 0};
   if (int rc = run_f(aq, st)) return rc;
   // d = dv = 64 bf16: dK and dV in one fused reverse scan (sweep 2, kernel.py:207-231)
-  static const bool no_fused = std::getenv("LA2_NO_FUSED_BWD") != nullptr;
-  if (dtype == LA2_BF16 && d == 64 && dvd == 64 && !no_fused)
+  // (experimental single-kernel dK/dV scan, la2_bwd.cu; opt-in: slower than the pair below)
+  static const bool fused_g = std::getenv("LA2_FUSED_BWD_G") != nullptr;
+  if (fused_g && dtype == LA2_BF16 && d == 64 && dvd == 64)
     return launch_g(q, k, v, dout, dk, dv, decay, dkv_in, dkv_out, B, H, N, st);
+  if (dtype == LA2_BF16 && d == 64 && dvd == 64) {
+    // dV and dK scans as one cluster pair sharing the Q and dO tiles (sweep 2, kernel.py:207-231)
+    FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
+    FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+    return launch_tc_pair(av, ak, st);
+  }
   // dK = F_rev(V, dO, Q): reverse scan, state dKV^T  (sweep 2, kernel.py:207-216)
   FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
   if (int rc = run_f(ak, st)) return rc;

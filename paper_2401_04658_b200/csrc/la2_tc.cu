@@ -30,6 +30,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "la2_tc_common.cuh"
 
@@ -74,12 +75,24 @@ struct TcLayout {
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
-template <int DK, bool REV, bool SO>
+// Cluster modes (2-CTA clusters along blockIdx.x; shared tiles are loaded once and
+// multicast, stage release collects both CTAs' MMA commits):
+//   CM = 0  no cluster
+//   CM = 1  value-slice pair: both CTAs use the same Q and K tiles (rank 0 loads Q,
+//           rank 1 loads K), each loads its own 64-column V slice
+//   CM = 2  backward pair: rank 0 runs F_rev(K, Q, dO) -> dV, rank 1 runs
+//           F_rev(V, dO, Q) -> dK; the Q and dO tiles are shared (rank 0 loads Q,
+//           rank 1 loads dO) and play swapped k/v roles in the two CTAs
+template <int DK, bool REV, bool SO, int CM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     la2_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                  const __grid_constant__ CUtensorMap tm_q1, const __grid_constant__ CUtensorMap tm_o1,
                   const FParams p) {
   using L = TcLayout<DK, SO>;
+  constexpr bool CL = (CM != 0);
+  static_assert(CM != 2 || (DK == 64 && REV && !SO), "backward pair needs d = dv = 64");
+  static_assert(!(CL && SO), "state-only passes run without clusters");
   constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -88,7 +101,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int slice = blockIdx.x;
+  const uint32_t crank = CL ? cluster_ctarank() : 0;
+  const bool sib = (CM == 2) && (crank == 1);      // sibling pass of the backward pair
+  const CUtensorMap* mq = sib ? &tm_q1 : &tm_q;
+  const CUtensorMap* mo = sib ? &tm_o1 : &tm_o;
+  const int offk = sib ? L::OFF_V : L::OFF_K;       // this CTA's k tile region
+  const int offv = sib ? L::OFF_K : L::OFF_V;       // this CTA's v tile region
+  const int kv_in_T = sib ? 1 : p.kv_in_T;          // the dK pass carries dKV^T
+  float* const kv_out = sib ? nullptr : p.kv_out;
+  const int slice = (CM == 2) ? 0 : blockIdx.x;
   const int h = blockIdx.y;
   const int bh = blockIdx.z * p.H + h;
   const int N = p.N;
@@ -97,7 +118,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[L::B_FULL + s], 1);
-      mbar_init(&bars[L::B_EMPTY + s], SO ? 1 : 2);  // X after PV, Y after Oe
+      // X after PV, Y after Oe (x2 in a cluster: the stage is shared)
+      mbar_init(&bars[L::B_EMPTY + s], (SO ? 1 : 2) * (CL ? 2 : 1));
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[L::B_SFULL + b], 1);
@@ -119,14 +141,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    if (!SO) tma_prefetch_desc(&tm_q);
+    if (!SO) tma_prefetch_desc(mq);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
-    if (!SO) tma_prefetch_desc(&tm_o);
+    if (!SO) tma_prefetch_desc(mo);
   }
   if (warp == 1) tmem_alloc(tmem_slot, L::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if (CL) cluster_sync();  // barriers initialised in both CTAs before any remote traffic
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -142,14 +165,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ahead, which exposes HBM latency; pull the next PF blocks into L2 so the ring's
       // TMA loads hit L2.
       constexpr int PF = (NS == 2) ? 3 : 0;
-      auto prefetch = [&](int i) {
+      auto prefetch = [&](int i) {  // the tiles this CTA itself fetches
         const int b2 = REV ? (nblk - 1 - i) : i;
+        if (CM == 0) {
 #pragma unroll
-        for (int c = 0; c < DK / 64; ++c) {
-          if (!SO) tma_prefetch_l2_3d(&tm_q, c * 64, b2 * BT, bh);
-          tma_prefetch_l2_3d(&tm_k, c * 64, b2 * BT, bh);
+          for (int c = 0; c < DK / 64; ++c) {
+            if (!SO) tma_prefetch_l2_3d(mq, c * 64, b2 * BT, bh);
+            tma_prefetch_l2_3d(&tm_k, c * 64, b2 * BT, bh);
+          }
+          tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
+        } else if (CM == 1) {
+#pragma unroll
+          for (int c = 0; c < DK / 64; ++c) tma_prefetch_l2_3d(crank ? &tm_k : &tm_q, c * 64, b2 * BT, bh);
+          tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
+        } else {
+          tma_prefetch_l2_3d(mq, 0, b2 * BT, bh);
+          tma_prefetch_l2_3d(crank ? &tm_v : &tm_k, 0, b2 * BT, bh);
         }
-        tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
       };
       for (int i = NS; i < NS + PF && i < nblk; ++i) prefetch(i);
       for (int i = 0; i < nblk; ++i) {
@@ -161,16 +193,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         TR(0, i, 1);
         mbar_arrive_expect_tx(&bars[L::B_FULL + s], L::STAGE_TX);
         const int row = blk * BT;
+        uint64_t* fb = &bars[L::B_FULL + s];
+        uint8_t* dq = smem + L::OFF_Q + s * L::Q_BYTES;
+        uint8_t* dk = smem + L::OFF_K + s * L::K_BYTES;   // stage region "K" (tile of tm_k)
+        uint8_t* dv = smem + L::OFF_V + s * L::V_BYTES;   // stage region "V" (tile of tm_v)
+        if (CM == 0) {
 #pragma unroll
-        for (int c = 0; c < DK / 64; ++c) {
-          if (!SO)
-            tma_load_3d(smem + L::OFF_Q + s * L::Q_BYTES + c * REGION, &tm_q,
-                        &bars[L::B_FULL + s], c * 64, row, bh);
-          tma_load_3d(smem + L::OFF_K + s * L::K_BYTES + c * REGION, &tm_k, &bars[L::B_FULL + s],
-                      c * 64, row, bh);
+          for (int c = 0; c < DK / 64; ++c) {
+            if (!SO) tma_load_3d(dq + c * REGION, mq, fb, c * 64, row, bh);
+            tma_load_3d(dk + c * REGION, &tm_k, fb, c * 64, row, bh);
+          }
+          tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
+        } else if (CM == 1) {
+#pragma unroll
+          for (int c = 0; c < DK / 64; ++c) {
+            if (crank == 0) tma_load_3d_mc(dq + c * REGION, &tm_q, fb, c * 64, row, bh, 0x3);
+            else tma_load_3d_mc(dk + c * REGION, &tm_k, fb, c * 64, row, bh, 0x3);
+          }
+          tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
+        } else {
+          tma_load_3d(dq, mq, fb, 0, row, bh);  // own q: K (rank 0) or V (rank 1)
+          if (crank == 0) tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K
+          else tma_load_3d_mc(dv, &tm_v, fb, 0, row, bh, 0x3);             // dO -> region V
         }
-        tma_load_3d(smem + L::OFF_V + s * L::V_BYTES, &tm_v, &bars[L::B_FULL + s], slice * DVS,
-                    row, bh);
+      }
+      if (CL) {
+        // every MMA of both CTAs that read this CTA's stages has committed
+        for (int i = (nblk > NS ? nblk - NS : 0); i < nblk; ++i)
+          mbar_wait(&bars[L::B_EMPTY + (i % NS)], (i / NS) & 1);
       }
     }
   } else if (warp == 1 || warp == WY) {
@@ -183,8 +233,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t tO = tbase + L::T_O, tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
     // descriptor bases (start address is in 16-byte units in the low bits)
     const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
-    const uint64_t dK0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
-    const uint64_t dV0 = sdesc_sw128(smem_u32(smem + L::OFF_V), REGION, 1024);
+    const uint64_t dK0 = sdesc_sw128(smem_u32(smem + offk), 16, 1024);
+    const uint64_t dV0 = sdesc_sw128(smem_u32(smem + offv), REGION, 1024);
+    auto commit_empty = [&](int s) {
+      if (CL) umma_commit_mc(&bars[L::B_EMPTY + s], 0x3);
+      else umma_commit(&bars[L::B_EMPTY + s]);
+    };
     const uint64_t dKT0 = sdesc_sw128(smem_u32(smem + L::OFF_KT), REGION, 1024);
     const uint64_t dKV0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), DK * 128, 1024);
     auto adv = [](uint64_t d, uint32_t bytes) { return d + static_cast<uint64_t>(bytes >> 4); };
@@ -227,7 +281,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                            ID_O, kk > 0);
             umma_commit(&bars[L::B_SFREE + b]);
             umma_commit(&bars[L::B_OFULLX]);
-            umma_commit(&bars[L::B_EMPTY + s]);
+            commit_empty(s);
           }
           __syncwarp();
         }
@@ -245,13 +299,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (leader) {
           // dKV = K^T (c . V): A = K^T (MN-major view of the K stage), B = V~ (MN-major)
           const uint64_t vt_d = adv(dKT0, kt * L::V_BYTES);
-          const uint64_t kA = sdesc_sw128(smem_u32(smem + L::OFF_K + s * L::K_BYTES), REGION, 1024);
+          const uint64_t kA = sdesc_sw128(smem_u32(smem + offk + s * L::K_BYTES), REGION, 1024);
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
             umma_bf16_ss(tKV + db * 64, adv(kA, kk * 2048), adv(vt_d, kk * 2048), ID_KV, kk > 0);
           umma_commit(&bars[L::B_DKVFULL + db]);
           umma_commit(&bars[L::B_KTFREE + kt]);
-          if (SO) umma_commit(&bars[L::B_EMPTY + s]);
+          if (SO) commit_empty(s);
         }
         __syncwarp();
         if (!SO) {
@@ -266,7 +320,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dKV0, kk * 2048),
                            ID_O, kk > 0);
             umma_commit(&bars[L::B_OEFULL]);
-            umma_commit(&bars[L::B_EMPTY + s]);
+            commit_empty(s);
           }
           __syncwarp();
         }
@@ -367,7 +421,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           named_bar_sync(1 + q4, 64);
           if (storer) {
-            tma_store_3d(&tm_o, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
+            tma_store_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
             tma_store_commit();
           }
           if (warp == 2) TR(2, i, 6);
@@ -390,7 +444,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
     if (p.kv_in != nullptr && has_kv) {
       const int c0 = slice * DVS;
-      if (!p.kv_in_T) {
+      if (!kv_in_T) {
         const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * dvt + c0;
 #pragma unroll
         for (int j = 0; j < DVS; j += 4) {
@@ -425,7 +479,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
         if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
         if (warp == W0) TR(3, j, 1);
-        scale_row_copy<64>(smem + L::OFF_V + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
+        scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
                            row, c);
         fence_proxy_async_smem();
         __syncwarp();
@@ -470,15 +524,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (warp == W0) TR(3, i, 5);
       }
     }
-    if (p.kv_out != nullptr && has_kv) {
-      float* dst = p.kv_out + sbase + static_cast<size_t>(kvrow) * dvt + slice * DVS;
+    if (kv_out != nullptr && has_kv) {
+      float* dst = kv_out + sbase + static_cast<size_t>(kvrow) * dvt + slice * DVS;
 #pragma unroll
       for (int j = 0; j < DVS; j += 4)
         *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL) cluster_sync();  // no remote arrivals / multicasts may target an exited CTA
+  else __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tbase, L::TMEM_COLS);
 }
@@ -516,29 +571,33 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r) - 1000;
 }
 
-template <int DK, bool REV, bool SO>
-static int launch_tc_t(const FArgs& a, cudaStream_t st) {
+template <int DK, bool REV, bool SO, int CM>
+static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullptr) {
   using L = TcLayout<DK, SO>;
-  auto kern = la2_tc_kernel<DK, REV, SO>;
+  auto kern = la2_tc_kernel<DK, REV, SO, CM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tc)", e);
-  CUtensorMap mq, mk, mv, mo;
+  if (CM != 0) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    (void)e;
+  }
+  CUtensorMap mq, mk, mv, mo, mq1, mo1;
   const int BH = a.B * a.H;
-  const void* ptrs[4] = {a.q, a.k, a.v, a.o};
-  CUtensorMap* maps[4] = {&mq, &mk, &mv, &mo};
-  const int cols[4] = {DK, DK, a.dv, a.dv};
-  for (int t = 0; t < 4; ++t) {
-    if (SO && (t == 0 || t == 3)) continue;
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, t == 3 ? 32 : BT);
+  const void* ptrs[6] = {a.q, a.k, a.v, a.o, a1 ? a1->q : a.q, a1 ? a1->o : a.o};
+  CUtensorMap* maps[6] = {&mq, &mk, &mv, &mo, &mq1, &mo1};
+  const int cols[6] = {DK, DK, a.dv, a.dv, DK, a.dv};
+  for (int t = 0; t < 6; ++t) {
+    if (SO && (t == 0 || t == 3 || t == 4 || t == 5)) continue;
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 5) ? 32 : BT);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),
-                    "cuTensorMapEncodeTiled failed for %c: CUresult %d (ptr=%p cols=%d N=%d BH=%d)",
-                    "qkvo"[t], -(rc + 1000), ptrs[t], cols[t], a.N, BH);
+                    "cuTensorMapEncodeTiled failed for operand %d: CUresult %d (ptr=%p cols=%d N=%d BH=%d)",
+                    t, -(rc + 1000), ptrs[t], cols[t], a.N, BH);
       return set_error(LA2_ERR_CUDA, buf);
     }
   }
-  if (SO) { mq = mk; mo = mv; }
+  if (SO) { mq = mk; mo = mv; mq1 = mk; mo1 = mv; }
   FParams p;
   p.N = a.N;
   p.H = a.H;
@@ -547,8 +606,20 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st) {
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
-  dim3 grid(a.dv / DVS, a.H, a.B);
-  kern<<<grid, TC_THREADS, L::TOTAL, st>>>(mq, mk, mv, mo, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CM == 2 ? 2 : a.dv / DVS, a.H, a.B);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CM ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CM ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mo1, p);
+  if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   return 0;
@@ -563,18 +634,40 @@ extern "C" LA2_API int la2_set_trace(long long* buf) {
 }
 #endif
 
+static bool clusters_enabled() {
+  static const bool off = std::getenv("LA2_NO_CLUSTER") != nullptr;
+  return !off;
+}
+
 int launch_tc(const FArgs& a, cudaStream_t st) {
   if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
   const bool so = (a.o == nullptr);
-  if (a.dk == 64) {
-    if (a.reverse) return so ? launch_tc_t<64, true, true>(a, st) : launch_tc_t<64, true, false>(a, st);
-    return so ? launch_tc_t<64, false, true>(a, st) : launch_tc_t<64, false, false>(a, st);
+  // value-slice pairs share their Q/K tiles through a 2-CTA cluster
+  const bool pair = !so && clusters_enabled() && (a.dv / DVS) % 2 == 0;
+#define LA2_TC_DISPATCH(DKV)                                                                   \
+  if (a.dk == DKV) {                                                                           \
+    if (so) return a.reverse ? launch_tc_t<DKV, true, true, 0>(a, st)                          \
+                             : launch_tc_t<DKV, false, true, 0>(a, st);                        \
+    if (pair) return a.reverse ? launch_tc_t<DKV, true, false, 1>(a, st)                       \
+                               : launch_tc_t<DKV, false, false, 1>(a, st);                     \
+    return a.reverse ? launch_tc_t<DKV, true, false, 0>(a, st)                                 \
+                     : launch_tc_t<DKV, false, false, 0>(a, st);                               \
   }
-  if (a.dk == 128) {
-    if (a.reverse) return so ? launch_tc_t<128, true, true>(a, st) : launch_tc_t<128, true, false>(a, st);
-    return so ? launch_tc_t<128, false, true>(a, st) : launch_tc_t<128, false, false>(a, st);
-  }
+  LA2_TC_DISPATCH(64)
+  LA2_TC_DISPATCH(128)
+#undef LA2_TC_DISPATCH
   return set_error(LA2_ERR_UNSUPPORTED, "tensor-core path supports head dim 64 or 128");
+}
+
+// The two reverse scans of the backward pass (dV = F_rev(K, Q, dO), dK = F_rev(V, dO, Q))
+// as one 2-CTA cluster per head sharing the Q and dO tiles. d = dv = 64, bf16.
+int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
+  if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
+  if (!clusters_enabled()) {
+    if (int rc = launch_tc_t<64, true, false, 0>(adk, st)) return rc;
+    return launch_tc_t<64, true, false, 0>(adv, st);
+  }
+  return launch_tc_t<64, true, false, 2>(adv, st, &adk);
 }
 
 }  // namespace la2
