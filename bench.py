@@ -180,11 +180,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=48)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c2 (default) = the headline BASELINE configs[1]; c1/c3/c4/c5 = the other configs")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload != "c2" and args.impl == "ours":
+        return extra_workload(args, world, rank, local_rank)
     B, H, N, D = args.batch, args.heads, args.seq_len, args.dim
     config = {"workload": "TransNormerLLM-400M attention (BASELINE configs[1]) fwd+bwd",
               "batch_per_gpu": B, "global_batch": B * world, "heads": H, "head_dim": D,
@@ -346,6 +350,146 @@ def main():
                 "config": config, "tflops": tflops, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": 4 * args.steps, "clocks": clk,
                 "sweep": sweep, "flatness": flat}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------- other BASELINE configs
+def extra_workload(args, world, rank, local_rank):
+    """c1: B=1 H=8 N=2048 d=64 (fp32 SIMT path + bf16);  c3: B=32 H=16 N=16K d=128
+    (B split over ranks: strong scaling);  c4: B=4 H=20 N=16K d=128 fwd+bwd plus
+    recurrent decode (batch 64, 256 graph-captured steps, fp32 state);  c5: one
+    512K-token sequence, H=16 d=128 -- intra-GPU sequence split on one GPU,
+    sequence parallel (one chunk per rank, state exchange over NCCL) under torchrun."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_04658_b200 as la2
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, tc_peak, peak_src = load_peaks()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps, warmup=3):
+        for _ in range(warmup):
+            fn()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / steps)
+
+    def rand(shape, dtype, seed):
+        g = torch.Generator(device=dev).manual_seed(seed + 1000 * rank)
+        return (torch.rand(*shape, device=dev, generator=g) * 2 - 1).to(dtype)
+
+    w = args.workload
+    line = {"n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "higher_is_better": True,
+            "vs_baseline": None, "data": "synthetic", "peak_source": peak_src}
+    clocks = ClockSampler(local_rank).start()
+    if w in ("c1", "c3", "c4"):
+        if w == "c1":
+            B, H, N, D, dtypes = 1, 8, 2048, 64, (torch.float32, torch.bfloat16)
+            decay = [0.5, 0.8, 0.9, 0.95, 0.99, 0.999, 0.9999, 1.0]
+        elif w == "c3":
+            B, H, N, D, dtypes = max(1, 32 // world), 16, 16384, 128, (torch.bfloat16,)
+            decay = alibi_decay(H)
+        else:
+            B, H, N, D, dtypes = 4, 20, 16384, 128, (torch.bfloat16,)
+            decay = alibi_decay(H)
+        dec = la2.decay_tensor(decay, H, dev)
+        results = {}
+        for dt in dtypes:
+            q, k, v, do = (rand((B, H, N, D), dt, i) for i in range(4))
+
+            q.requires_grad_(); k.requires_grad_(); v.requires_grad_()
+
+            def step():
+                q.grad = k.grad = v.grad = None  # gradients are written, not accumulated
+                o = la2.lightning_attn2(q, k, v, dec)
+                o.backward(do)
+            ms = timed(step, args.steps)
+            ff, fb = canonical_flops(N, D, D)
+            bf, bb = canonical_bytes(N, D, D, e=2 if dt == torch.bfloat16 else 4)
+            results[str(dt).split(".")[-1]] = {
+                "ms_per_step": ms, "tokens_per_s": B * N * world / (ms / 1e3),
+                "tflops": (ff + fb) * B * H * world / (ms / 1e3) / 1e12,
+                "frac_of_roof": max((ff + fb) * B * H / (tc_peak * 1e12), (bf + bb) * B * H / (hbm_peak * 1e9)) * 1e3 / ms}
+            q.grad = k.grad = v.grad = None
+            del q, k, v, do
+        main_dt = "bfloat16" if "bfloat16" in results else "float32"
+        line.update({"metric": f"{w} fwd+bwd tokens/s", "value": results[main_dt]["tokens_per_s"],
+                     "unit": UNIT, "ms_per_step": results[main_dt]["ms_per_step"],
+                     "scaling": "strong" if w == "c3" else "weak", "dtype": "bf16" if main_dt == "bfloat16" else "fp32",
+                     "config": {"workload": w, "batch_per_gpu": B, "heads": H, "seq_len": N, "head_dim": D,
+                                "api": "lightning_attn2 autograd"},
+                     "per_dtype": results})
+        if w == "c4":
+            Bd, steps_d = 64, 256
+            st0 = torch.zeros(Bd, H, D, D, device=dev)
+            qd, kd, vd = (rand((steps_d, Bd, H, D), torch.bfloat16, 10 + i) for i in range(3))
+            st = st0.clone()
+            la2.decode_step(qd[0], kd[0], vd[0], dec, st)  # warm the launch path
+            graph = torch.cuda.CUDAGraph()
+            st.copy_(st0)
+            with torch.cuda.graph(graph):
+                for t in range(steps_d):
+                    la2.decode_step(qd[t], kd[t], vd[t], dec, st)
+            ms_d = timed(graph.replay, max(3, args.steps // 4), 2)
+            state_bytes = Bd * H * D * D * 4 * 2
+            line["decode"] = {"batch": Bd, "steps_per_graph": steps_d, "ms_per_graph": ms_d,
+                              "tokens_per_s": Bd * steps_d * world / (ms_d / 1e3),
+                              "state_gbs": state_bytes * steps_d / (ms_d / 1e3) / 1e9,
+                              "frac_of_hbm": state_bytes * steps_d / (ms_d / 1e3) / 1e9 / hbm_peak}
+    else:  # c5
+        H, D, N_total = 16, 128, 524288
+        L = N_total // world
+        dec = la2.decay_tensor([min(1.0, x) for x in alibi_decay(H)], H, dev)
+        q, k, v, do = (rand((1, H, L, D), torch.bfloat16, i) for i in range(4))
+        q.requires_grad_(); k.requires_grad_(); v.requires_grad_()
+        if world == 1:
+            g = la2.split_factor(1, H, L, D, D, torch.bfloat16)
+
+            def step():
+                q.grad = k.grad = v.grad = None
+                o = la2.lightning_attn2(q, k, v, dec)
+                o.backward(do)
+            mode = f"intra-GPU sequence split x{g}"
+        else:
+            def step():
+                q.grad = k.grad = v.grad = None
+                o = la2.sp_lightning_attn2(q, k, v, dec, mode=os.environ.get("LA2_SP_MODE", "allgather"))
+                o.backward(do)
+            mode = f"sequence parallel x{world} ({os.environ.get('LA2_SP_MODE', 'allgather')}) "
+        ms = timed(step, args.steps)
+        ff, fb = canonical_flops(N_total, D, D)
+        bf, bb = canonical_bytes(N_total, D, D)
+        line.update({"metric": "c5 fwd+bwd tokens/s (one 512K sequence)", "value": N_total / (ms / 1e3),
+                     "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "dtype": "bf16",
+                     "config": {"workload": "c5", "seq_len": N_total, "heads": H, "head_dim": D,
+                                "per_rank_tokens": L, "mode": mode},
+                     "tflops": (ff + fb) * H / (ms / 1e3) / 1e12,
+                     "frac_of_roof": max((ff + fb) * H / (tc_peak * 1e12 * world),
+                                         (bf + bb) * H / (hbm_peak * 1e9 * world)) * 1e3 / ms})
+    line["clocks"] = clocks.stop()
+    if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -22,6 +22,9 @@ from .ops import (
     la2_backward,
     la2_forward,
     lightning_attn2,
+    split_backward,
+    split_factor,
+    split_forward,
     state_scan,
 )
 from .sp import exclusive_scan, sp_lightning_attn2
@@ -39,5 +42,8 @@ __all__ = [
     "la2_forward",
     "lightning_attn2",
     "sp_lightning_attn2",
+    "split_backward",
+    "split_factor",
+    "split_forward",
     "state_scan",
 ]

@@ -47,27 +47,21 @@ static int check_common(int B, int H, int N, int d, int dv, int dtype, const flo
   return 0;
 }
 
-// Make this library's runtime current on the device that owns the caller's
-// stream (or, for the legacy default stream, the device of a data pointer).
-// The library links its own static cudart, so torch's current device does not
-// carry over.
+// Make this library's runtime current on the device that owns the caller's data.
+// The library links its own static cudart, so torch's current device does not carry
+// over. (The device comes from the pointer rather than the stream: stream queries
+// are not permitted while the caller captures a CUDA graph.)
 static int bind_device(void* stream, const void* ptr) {
-  int dev = -1;
-  if (stream != nullptr) {
-    cudaError_t e = cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev);
-    if (e != cudaSuccess) return set_cuda_error("cudaStreamGetDevice", e);
-  } else {
-    cudaPointerAttributes at{};
-    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
-    if (e != cudaSuccess) return set_cuda_error("cudaPointerGetAttributes", e);
-    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
-      return set_error(LA2_ERR_VALUE, "tensor pointer is not device memory");
-    dev = at.device;
-  }
+  (void)stream;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) return set_cuda_error("cudaPointerGetAttributes", e);
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return set_error(LA2_ERR_VALUE, "tensor pointer is not device memory");
   int cur = -1;
   cudaGetDevice(&cur);
-  if (cur != dev) {
-    cudaError_t e = cudaSetDevice(dev);
+  if (cur != at.device) {
+    e = cudaSetDevice(at.device);
     if (e != cudaSuccess) return set_cuda_error("cudaSetDevice", e);
   }
   return 0;

@@ -97,6 +97,76 @@ def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name) -> Optional[tor
     return t.to(device=device, dtype=torch.float32).contiguous()
 
 
+# ------------------------------------------------------ intra-GPU sequence split
+NUM_SMS = 148
+
+
+def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
+    """Chunks per sequence for the intra-GPU split (1 = no split).
+
+    One CTA owns one (b, h, 64-wide value slice) for the whole sequence, so with
+    fewer units than SMs the GPU idles. Viewing [B,H,N,d] as [B,H*G,N/G,d] (a free
+    reshape) gives G x more units at the cost of one state-only pass over K,V (and
+    Q,dO in the backward). Used when units < ~100 and chunks stay >= 2048 tokens.
+    """
+    if dtype != torch.bfloat16 or d not in (64, 128) or dv % 64:
+        return 1
+    units = B * H * (dv // 64)
+    if units >= 100:
+        return 1
+    g = 1
+    while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 2048:
+        g *= 2
+    return g
+
+
+def _chunked(t: torch.Tensor, g: int) -> torch.Tensor:
+    B, H, N, c = t.shape
+    return t.view(B, H * g, N // g, c)
+
+
+def _to_chunk_major(st: torch.Tensor, B: int, H: int, g: int) -> torch.Tensor:
+    """[B, H*g, d, dv] -> [g, B, H, d, dv] (contiguous) for la2_state_scan."""
+    d, dv = st.shape[-2:]
+    return st.view(B, H, g, d, dv).permute(2, 0, 1, 3, 4).contiguous()
+
+
+def _from_chunk_major(st: torch.Tensor, B: int, H: int, g: int) -> torch.Tensor:
+    d, dv = st.shape[-2:]
+    return st.permute(1, 2, 0, 3, 4).reshape(B, H * g, d, dv).contiguous()
+
+
+def split_forward(q, k, v, decay, g: int, kv_in=None, output_final_state=False):
+    """Forward with the sequence cut into g chunks per (b, h). Returns
+    ``(o, kv_out, prefix)``; prefix (chunk-carried states) is reused by the backward."""
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    dec = decay_tensor(decay, H, q.device)
+    dec_g = dec.repeat_interleave(g)
+    q4, k4, v4 = _chunked(q.contiguous(), g), _chunked(k.contiguous(), g), _chunked(v.contiguous(), g)
+    s = chunk_state(k4, v4, dec_g)
+    init = None if kv_in is None else _state(kv_in, B, H, d, dv, q.device, "kv_in")
+    prefix = _from_chunk_major(state_scan(_to_chunk_major(s, B, H, g), dec, [N // g] * g, init=init), B, H, g)
+    o4, kv4 = la2_forward(q4, k4, v4, dec_g, kv_in=prefix, output_final_state=output_final_state)
+    kv_out = None if kv4 is None else kv4.view(B, H, g, d, dv)[:, :, -1].contiguous()
+    return o4.view(B, H, N, dv), kv_out, prefix
+
+
+def split_backward(q, k, v, d_out, decay, g: int, prefix, dkv_in=None, output_dkv=False):
+    """Backward matching :func:`split_forward` (prefix = its chunk-carried states)."""
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    dec = decay_tensor(decay, H, q.device)
+    dec_g = dec.repeat_interleave(g)
+    q4, k4, v4, do4 = (_chunked(t.contiguous(), g) for t in (q, k, v, d_out))
+    t = chunk_dstate(q4, do4, dec_g)
+    init = None if dkv_in is None else _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
+    suffix = _from_chunk_major(state_scan(_to_chunk_major(t, B, H, g), dec, [N // g] * g, init=init,
+                                          reverse=True), B, H, g)
+    dq, dk, dvv, dkv4 = la2_backward(q4, k4, v4, do4, dec_g, kv_in=prefix, dkv_in=suffix,
+                                     output_dkv=output_dkv)
+    dkv_out = None if dkv4 is None else dkv4.view(B, H, g, d, dv)[:, :, 0].contiguous()
+    return dq.view(B, H, N, d), dk.view(B, H, N, d), dvv.view(B, H, N, dv), dkv_out
+
+
 # ------------------------------------------------------------------ raw passes
 def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
                 output_final_state: bool = False):
@@ -210,10 +280,18 @@ class LightningAttn2Fn(torch.autograd.Function):
     the reference's backward (pkg/src/tila/kernel.py:184-204)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, decay, initial_state, output_final_state):
-        o, kv_out = la2_forward(q, k, v, decay, kv_in=initial_state,
-                                output_final_state=output_final_state)
-        ctx.save_for_backward(q, k, v, decay, initial_state)
+    def forward(ctx, q, k, v, decay, initial_state, output_final_state, seq_split):
+        B, H, N, d = q.shape
+        g = split_factor(B, H, N, d, v.shape[3], q.dtype) if seq_split == "auto" else int(seq_split)
+        if g > 1:
+            o, kv_out, prefix = split_forward(q, k, v, decay, g, kv_in=initial_state,
+                                              output_final_state=output_final_state)
+        else:
+            o, kv_out = la2_forward(q, k, v, decay, kv_in=initial_state,
+                                    output_final_state=output_final_state)
+            prefix = None
+        ctx.g = g
+        ctx.save_for_backward(q, k, v, decay, initial_state, prefix)
         ctx.set_materialize_grads(False)
         ctx.want_state_grad = initial_state is not None and initial_state.requires_grad
         if kv_out is None:
@@ -222,17 +300,22 @@ class LightningAttn2Fn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, d_o, *rest):
-        q, k, v, decay, initial_state = ctx.saved_tensors
+        q, k, v, decay, initial_state, prefix = ctx.saved_tensors
         d_final = rest[0] if rest else None
         if d_o is None:
             d_o = torch.zeros_like(v)
-        dq, dk, dv, dkv = la2_backward(q, k, v, d_o.to(q.dtype), decay, kv_in=initial_state,
-                                       dkv_in=d_final, output_dkv=ctx.want_state_grad)
-        return dq, dk, dv, None, dkv, None
+        if ctx.g > 1:
+            dq, dk, dv, dkv = split_backward(q, k, v, d_o.to(q.dtype).contiguous(), decay, ctx.g, prefix,
+                                             dkv_in=d_final, output_dkv=ctx.want_state_grad)
+        else:
+            dq, dk, dv, dkv = la2_backward(q, k, v, d_o.to(q.dtype), decay, kv_in=initial_state,
+                                           dkv_in=d_final, output_dkv=ctx.want_state_grad)
+        return dq, dk, dv, None, dkv, None, None
 
 
 def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: DecayLike,
-                    initial_state: Optional[torch.Tensor] = None, output_final_state: bool = False):
+                    initial_state: Optional[torch.Tensor] = None, output_final_state: bool = False,
+                    seq_split="auto"):
     """Causal linear attention with per-head exponential decay, on the GPU.
 
     Args:
@@ -240,6 +323,8 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
       decay: per-head lambda in (0, 1] -- float, sequence of H floats or a tensor.
       initial_state: optional fp32 ``[B, H, d, dv]`` state carried in.
       output_final_state: also return the fp32 final state.
+      seq_split: "auto" (split long sequences into chunks when B*H is too small to
+        fill the GPU, see :func:`split_factor`) or an explicit chunk count (1 = off).
     Returns ``o`` (``[B,H,N,dv]``, input dtype), or ``(o, final_state)``.
     """
     _check_qkv(q, k, v)
@@ -250,4 +335,4 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
             raise ValueError(f"initial_state must have shape {(B, H, d, v.shape[3])}")
         if initial_state.dtype != torch.float32:
             initial_state = initial_state.float()
-    return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state))
+    return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state), seq_split)

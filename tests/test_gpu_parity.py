@@ -340,3 +340,51 @@ def test_unsupported_shapes_raise():
     q = torch.zeros(1, 1, 8, 64, device=DEV, dtype=torch.float16)
     with pytest.raises(ValueError):
         la2.la2_forward(q, q, q, 0.9)
+
+
+# ------------------------------------------------------ intra-GPU sequence split
+@pytest.mark.parametrize("g,d", [(4, 64), (8, 128)])
+def test_sequence_split_matches_reference(g, d):
+    """[B,H,N,d] viewed as [B,H*g,N/g,d]: chunk states, scans, carried-state passes
+    (forward and backward, with incoming states) == the unsplit reference."""
+    B, H, N = 1, 2, 4096
+    decay = [0.999, 1.0]
+    q, k, v, do = inputs(B, H, N, d, d, torch.bfloat16, seed=91 + d)
+    init = torch.randn(B, H, d, d) * 0.05
+    dinit = torch.randn(B, H, d, d) * 0.05
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    o, kv_out, prefix = la2.split_forward(*gpu(q, k, v), decay, g, kv_in=init.to(DEV), output_final_state=True)
+    dq, dk, dv_, dkv = la2.split_backward(*gpu(q, k, v, do), decay, g, prefix, dkv_in=dinit.to(DEV),
+                                          output_dkv=True)
+    ro, rkv = port.bhnd_forward(Q, K, V, decay, kv_in=init.double().numpy())
+    # references with carried states: embed the incoming dkv through the suffix identity
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
+    DI, I0 = dinit.double().numpy(), init.double().numpy()
+    for h in range(H):
+        lam = decay[h]
+        read = lam ** (np.arange(N) + 1.0)
+        write = lam ** (N - 1.0 - np.arange(N))
+        rq[0, h] += (DO[0, h] * read[:, None]) @ I0[0, h].T
+        rk[0, h] += (V[0, h] * write[:, None]) @ DI[0, h].T
+        rv[0, h] += (K[0, h] * write[:, None]) @ DI[0, h]
+    rdkv = _suffix_dstate(Q, DO, decay, 0) + np.stack([[decay[h] ** N * DI[0, h] for h in range(H)]])
+    errs = {"o": rel(o, ro), "kv": rel(kv_out, rkv), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv),
+            "dkv": rel(dkv, rdkv)}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_autograd_auto_split():
+    """lightning_attn2 picks the split automatically for few heads and long N."""
+    B, H, N, D = 1, 2, 16384, 128
+    assert la2.split_factor(B, H, N, D, D, torch.bfloat16) > 1
+    decay = [0.9999, 1.0]
+    q, k, v, do = inputs(B, H, N, D, D, torch.bfloat16, seed=123)
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    o = la2.lightning_attn2(qg, kg, vg, decay)
+    o.backward(do.to(DEV))
+    o1 = la2.lightning_attn2(*gpu(q, k, v), decay, seq_split=1)
+    ro, _ = port.bhnd_forward(to64(q), to64(k), to64(v), decay, block=256)
+    rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay, block=256)
+    errs = {"o": rel(o, ro), "o_nosplit": rel(o1, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk),
+            "dv": rel(vg.grad, rv)}
+    assert max(errs.values()) <= BF16_TOL, errs
