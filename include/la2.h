@@ -116,6 +116,22 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
                     float* state, void* o, int B, int H, int d, int dv, int dtype, void* stream);
 
 /*
+ * Scheduling knobs of the tensor-core kernels (process-wide; not a reference
+ * interface). Results do not depend on them: the persistent schedule hands the fp32
+ * state between work ranges exactly, so outputs are bitwise identical either way.
+ *   LA2_TUNE_PERSISTENT  1 (default): when there are more recurrences than co-resident
+ *                        CTAs, run one persistent CTA per SM over an even split of the
+ *                        (recurrence, block) space; 0: one CTA per recurrence.
+ *   LA2_TUNE_PREFETCH    L2 prefetch distance in blocks for 2-stage rings (default 1).
+ *   LA2_TUNE_L2HINT      L2 policy bits: 1 loads evict_first, 2 prefetches evict_last,
+ *                        4 output stores evict_first (default 3).
+ */
+#define LA2_TUNE_PERSISTENT 1
+#define LA2_TUNE_PREFETCH 2
+#define LA2_TUNE_L2HINT 3
+LA2_API int la2_set_tuning(int key, int value);
+
+/*
  * Self-test of the tensor-core operand layouts (not a reference replacement):
  * D[M][N] = A[M][K] B[K][N] through the same SW128 descriptors the tcgen05
  * kernel uses; a_mn / b_mn select MN-major staging. fp32 device buffers.

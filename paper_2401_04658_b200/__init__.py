@@ -22,6 +22,7 @@ from .ops import (
     la2_backward,
     la2_forward,
     lightning_attn2,
+    set_tuning,
     split_backward,
     split_factor,
     split_forward,
@@ -41,6 +42,7 @@ __all__ = [
     "la2_backward",
     "la2_forward",
     "lightning_attn2",
+    "set_tuning",
     "sp_lightning_attn2",
     "split_backward",
     "split_factor",

@@ -34,11 +34,13 @@ SIGNATURES: dict[str, list] = {
     "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "la2_set_tuning": [_i, _i],
     "la2_selftest_umma": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_bench_umma": [_i, _i, _i, _i, _i, _i, _vp, _vp],
     "la2_bench_tmem": [_i, _i, _i, _i, _vp, _vp, _vp],
 }
 _RESTYPES = {"la2_last_error": ctypes.c_char_p}
+_DEV_ONLY = {"la2_set_tuning", "la2_selftest_umma", "la2_bench_umma", "la2_bench_tmem"}
 
 _lib = None
 
@@ -54,6 +56,8 @@ def load() -> ctypes.CDLL:
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(str(LIB_PATH))
     for name, args in SIGNATURES.items():
+        if name in _DEV_ONLY and not hasattr(lib, name):
+            continue  # development entry points (older or trimmed builds)
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _RESTYPES.get(name, ctypes.c_int)

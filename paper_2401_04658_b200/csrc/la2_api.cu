@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "la2_kernels.h"
 
@@ -18,6 +20,47 @@ int set_error(int code, const char* msg) {
 int set_cuda_error(const char* where, cudaError_t e) {
   std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
   return LA2_ERR_CUDA;
+}
+
+// Handoff workspace of the persistent schedule, one per (device, stream) so that
+// kernels on different streams never share flags. Allocated once, zeroed, never freed;
+// the flags return to zero at the end of every launch (each is consumed by its reader).
+Workspace get_workspace(cudaStream_t st) {
+  struct Entry {
+    int dev;
+    cudaStream_t st;
+    Workspace w;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return Workspace{nullptr, nullptr, 0};
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache)
+    if (e.dev == dev && e.st == st) return e.w;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return Workspace{nullptr, nullptr, 0};
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int slots = sms;  // at most one CTA per SM
+  const size_t state_bytes = static_cast<size_t>(slots) * 128 * 64 * sizeof(float);
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, state_bytes + slots * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    return Workspace{nullptr, nullptr, 0};
+  }
+  int* flags = reinterpret_cast<int*>(static_cast<char*>(buf) + state_bytes);
+  if (cudaMemset(flags, 0, slots * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(buf);
+    return Workspace{nullptr, nullptr, 0};
+  }
+  Workspace w{static_cast<float*>(buf), flags, slots};
+  cache.push_back(Entry{dev, st, w});
+  return w;
 }
 
 static bool tc_eligible(int dtype, int dk, int dv) {
@@ -76,6 +119,11 @@ extern "C" {
 int la2_version(void) { return 100; }
 
 const char* la2_last_error(void) { return g_err; }
+
+int la2_set_tuning(int key, int value) {
+  g_err[0] = 0;
+  return set_tuning(key, value);
+}
 
 int la2_forward(const void* q, const void* k, const void* v, const float* decay, void* o,
                 const float* kv_in, float* kv_out, int B, int H, int N, int d, int dv, int dtype,

@@ -33,6 +33,12 @@ struct FParams {
   int kv_in_T;
   float* kv_out;
   int dv_total;
+  int pf;    // L2 prefetch distance in blocks (2-stage rings)
+  int hint;  // L2 cache-policy bits: 1 loads evict_first, 2 prefetch evict_last, 4 stores evict_first
+  // persistent schedule (tensor-core kernels): `units` recurrences over P work ranges
+  int units, P, nsl;
+  float* ws;   // [P * cluster][dk][64] fp32 state handoff between neighbouring ranges
+  int* flags;  // [P * cluster] handoff flags (0 = empty), reset by their reader
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);
@@ -52,6 +58,16 @@ int launch_state_scan(const float* chunk_states, const float* decay, const float
                       float* prefix, int G, int BH, int H, int dk, int dv, const int* lens,
                       int reverse, cudaStream_t st);
 
+// Per-(device, stream) handoff workspace for the persistent schedule; nullptr when it
+// cannot be allocated (e.g. first use inside a CUDA graph capture).
+struct Workspace {
+  float* ws;
+  int* flags;
+  int slots;
+};
+Workspace get_workspace(cudaStream_t st);
+
+int set_tuning(int key, int value);
 int set_error(int code, const char* msg);
 int set_cuda_error(const char* where, cudaError_t e);
 

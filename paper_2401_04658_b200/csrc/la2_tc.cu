@@ -59,7 +59,8 @@ struct TcLayout {
   static constexpr int OFF_O = OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int TOTAL = OFF_BAR + BAR_BYTES + 1024;  // + alignment slack
+  static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
+  static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
   // TMEM columns: S[2] @0,128 (P aliased) | O @256 | Oe @320 | dKV[2] @384,448
   // (state-only: dKV[2] @0,64)
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   const FParams p) {
   using L = TcLayout<DK, SO>;
   constexpr bool CL = (CM != 0);
+  constexpr int CS = CL ? 2 : 1;  // CTAs per cluster
   static_assert(CM != 2 || (DK == 64 && REV && !SO), "backward pair needs d = dv = 64");
   static_assert(!(CL && SO), "state-only passes run without clusters");
   constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::B_COUNT);
+  BlkRec* recs = reinterpret_cast<BlkRec*>(smem + L::OFF_REC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -109,11 +112,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int offv = sib ? L::OFF_K : L::OFF_V;       // this CTA's v tile region
   const int kv_in_T = sib ? 1 : p.kv_in_T;          // the dK pass carries dKV^T
   float* const kv_out = sib ? nullptr : p.kv_out;
-  const int slice = (CM == 2) ? 0 : blockIdx.x;
-  const int h = blockIdx.y;
-  const int bh = blockIdx.z * p.H + h;
   const int N = p.N;
   const int nblk = (N + BT - 1) / BT;
+  const int cid = blockIdx.x / CS;                  // this CTA's (cluster's) work range
+  Sched sch;
+  sch.init(cid, p.P, p.units, nblk);
+  const int T = sch.T;
+  const int nsl = p.nsl, H = p.H, cr = static_cast<int>(crank);
+  auto blk_of = [&](int pos) { return REV ? (nblk - 1 - pos) : pos; };
+  // exact log2 of the head's decay (fast-math log2f is off by ~2^-22 absolute, which
+  // compounds over 64K tokens when lam is close to 1)
+  auto log2_decay = [&](int h) {
+    const float lam = p.decay[h];
+    return (lam >= 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -153,20 +165,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  const float lam = p.decay[h];
-  // exact log2 (fast-math log2f is off by ~2^-22 absolute, which compounds over
-  // 64K tokens when lam is close to 1)
-  const float l2 = (lam >= 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
-
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       // With a 2-stage ring (d = 128: 80 KB stages) a stage is refilled only one block
       // ahead, which exposes HBM latency; pull the next PF blocks into L2 so the ring's
       // TMA loads hit L2.
-      constexpr int PF = (NS == 2) ? 3 : 0;
-      auto prefetch = [&](int i) {  // the tiles this CTA itself fetches
-        const int b2 = REV ? (nblk - 1 - i) : i;
+      const int PF = (NS == 2) ? p.pf : 0;
+      const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+      auto tma_prefetch_l2_3d = [&](const CUtensorMap* m, int c0, int c1, int c2) {
+        if (p.hint & 2) la2::tma_prefetch_l2_3d_hint(m, c0, c1, c2, pol_last);
+        else la2::tma_prefetch_l2_3d(m, c0, c1, c2);
+      };
+      auto tma_load_3d = [&](void* d, const CUtensorMap* m, uint64_t* b, int c0, int c1, int c2) {
+        if (p.hint & 1) la2::tma_load_3d_hint(d, m, b, c0, c1, c2, pol_first);
+        else la2::tma_load_3d(d, m, b, c0, c1, c2);
+      };
+      auto tma_load_3d_mc = [&](void* d, const CUtensorMap* m, uint64_t* b, int c0, int c1, int c2,
+                                uint16_t mask) {
+        if (p.hint & 1) la2::tma_load_3d_mc_hint(d, m, b, c0, c1, c2, mask, pol_first);
+        else la2::tma_load_3d_mc(d, m, b, c0, c1, c2, mask);
+      };
+      Walk<CM> pw;  // the block PF ahead of the ring
+      pw.start(sch, NS, nsl, H, cr);
+      auto prefetch = [&]() {  // the tiles this CTA itself fetches for block pw.g
+        const int bh = pw.bh, slice = pw.slice, b2 = blk_of(pw.pos);
+        pw.next(sch, nsl, H, cr);
         if (CM == 0) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
@@ -183,14 +207,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tma_prefetch_l2_3d(crank ? &tm_v : &tm_k, 0, b2 * BT, bh);
         }
       };
-      for (int i = NS; i < NS + PF && i < nblk; ++i) prefetch(i);
-      for (int i = 0; i < nblk; ++i) {
-        if (PF > 0 && i + NS + PF < nblk) prefetch(i + NS + PF);
-        const int blk = REV ? (nblk - 1 - i) : i;
-        const int s = i % NS;
-        TR(0, i, 0);
-        if (i >= NS) mbar_wait(&bars[L::B_EMPTY + s], ((i / NS) - 1) & 1);
-        TR(0, i, 1);
+      for (int g = NS; g < NS + PF && g < T; ++g) prefetch();
+      Walk<CM> w;
+      w.start(sch, 0, nsl, H, cr);
+      const int suffix_start = sch.npre + sch.nfull * nblk;
+      int rec_h = -1;
+      float rec_l2 = 0.f;
+      for (int g = 0; g < T; ++g, w.next(sch, nsl, H, cr)) {
+        if (PF > 0 && g + NS + PF < T) prefetch();
+        const int bh = w.bh, slice = w.slice, blk = blk_of(w.pos);
+        const int s = g % NS;
+        TR(0, g, 0);
+        if (g >= NS) mbar_wait(&bars[L::B_EMPTY + s], ((g / NS) - 1) & 1);
+        TR(0, g, 1);
+        // Schedule record of block g for the row and state warps, published by the
+        // FULL arrive below (ring of 8 > the deepest lag any consumer can have).
+        if (w.h != rec_h) {
+          rec_h = w.h;
+          rec_l2 = log2_decay(w.h);
+        }
+        {
+          BlkRec rc;
+          rc.bh = bh;
+          rc.slice = slice;
+          rc.pos = w.pos;
+          rc.blk = blk;
+          rc.l2 = rec_l2;
+          rc.h = w.h;
+          rc.flags = ((w.pos == 0 || g == suffix_start) ? REC_SEG_START : 0) |
+                     ((w.pos == nblk - 1 || g == sch.npre - 1) ? REC_SEG_END : 0);
+          recs[g & 7] = rc;
+        }
         mbar_arrive_expect_tx(&bars[L::B_FULL + s], L::STAGE_TX);
         const int row = blk * BT;
         uint64_t* fb = &bars[L::B_FULL + s];
@@ -219,8 +266,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (CL) {
         // every MMA of both CTAs that read this CTA's stages has committed
-        for (int i = (nblk > NS ? nblk - NS : 0); i < nblk; ++i)
-          mbar_wait(&bars[L::B_EMPTY + (i % NS)], (i / NS) & 1);
+        for (int g = (T > NS ? T - NS : 0); g < T; ++g)
+          mbar_wait(&bars[L::B_EMPTY + (g % NS)], (g / NS) & 1);
       }
     }
   } else if (warp == 1 || warp == WY) {
@@ -262,12 +309,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           __syncwarp();
         };
-        issue_S(0);
-        for (int i = 0; i < nblk; ++i) {
+        if (T > 0) issue_S(0);
+        for (int i = 0; i < T; ++i) {
           const int s = i % NS, b = i & 1;
           const uint64_t v = adv(dV0, s * L::V_BYTES);
           TR(1, i, 0);
-          if (i + 1 < nblk) issue_S(i + 1);
+          if (i + 1 < T) issue_S(i + 1);
           TR(1, i, 1);
           mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
           TR(1, i, 2);
@@ -288,9 +335,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     } else {
       // ---- Y: state chain  dKV_i = K~_i^T V_i (early) ; Oe_i = Q_i KV_{i-1}
-      for (int i = 0; i < nblk; ++i) {
+      for (int i = 0; i < T; ++i) {
         const int s = i % NS, kt = i % KTS, db = i & 1;
-        const uint64_t v = adv(dV0, s * L::V_BYTES);
         mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
         if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
         mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
@@ -336,28 +382,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
       // Mask factors for this row and this warp's 4 chunks of 16 score columns:
       //   M[row][16ch + j] = (ch == dch) ? Dg[j] : F[ch] * G[j]   (F = 0 on the zero side)
+      // recomputed whenever the schedule moves to another head.
       float G[16], Dg[16], F[4];
       const int dch = row >> 4, tt = row & 15;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (!REV) {
-          G[j] = lam_pow(l2, 15 - j);
-          Dg[j] = (j <= tt) ? lam_pow(l2, tt - j) : 0.f;
-        } else {
-          G[j] = lam_pow(l2, j);
-          Dg[j] = (j >= tt) ? lam_pow(l2, j - tt) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int ch = 4 * half + c;
-        if (!REV) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
-        else F[c] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
-      }
-      for (int j = 0; j <= nblk; ++j) {
-        if (j < nblk) {
+      int mask_h = -1;
+      for (int j = 0; j <= T; ++j) {
+        if (j < T) {
           // ---- A(j): S -> P (bf16). This warp reads score columns [64h, 64h+64) and
           // writes the packed P pairs into columns [64h, 64h+32) of the same buffer.
+          mbar_wait(&bars[L::B_FULL + j % NS], (j / NS) & 1);  // record j is published
+          const BlkRec rc = recs[j & 7];
+          if (rc.h != mask_h) {
+            mask_h = rc.h;
+            const float l2 = rc.l2;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              if (!REV) {
+                G[jj] = lam_pow(l2, 15 - jj);
+                Dg[jj] = (jj <= tt) ? lam_pow(l2, tt - jj) : 0.f;
+              } else {
+                G[jj] = lam_pow(l2, jj);
+                Dg[jj] = (jj >= tt) ? lam_pow(l2, jj - tt) : 0.f;
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int ch = 4 * half + c;
+              if (!REV) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
+              else F[c] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
+            }
+          }
           const int b = j & 1;
           const uint32_t tS = tbase + b * 128 + half * 64 + lane_off;
           if (warp == 2) TR(2, j, 0);
@@ -389,9 +443,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (j >= 1) {
           // ---- B(j-1): o = O + a_t Oe for value columns [32h, 32h+32) -> smem -> TMA store
           const int i = j - 1;
-          const int blk = REV ? (nblk - 1 - i) : i;
+          // record i was acquired in A(i); the ring slot is not rewritten before B(i) ends
+          const BlkRec rb = recs[i & 7];
+          const int bh = rb.bh, slice = rb.slice, blk = rb.blk;
+          const float out_l2 = rb.l2;
           const int r = min(BT, N - blk * BT);
-          const float a = REV ? (row < r ? lam_pow(l2, r - 1 - row) : 0.f) : lam_pow(l2, row + 1);
+          const float a = REV ? (row < r ? lam_pow(out_l2, r - 1 - row) : 0.f) : lam_pow(out_l2, row + 1);
           uint8_t* sO = smem + L::OFF_O + (i % OS) * L::O_BYTES;
           const bool storer = (half == 0 && lane == 0);
           if (warp == 2) TR(2, i, 3);
@@ -421,7 +478,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           named_bar_sync(1 + q4, 64);
           if (storer) {
-            tma_store_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
+            if (p.hint & 4)
+              tma_store_3d_hint(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh,
+                                l2_policy_evict_first());
+            else
+              tma_store_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
             tma_store_commit();
           }
           if (warp == 2) TR(2, i, 6);
@@ -438,27 +499,74 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool has_kv = (DK == 128) || (lane < 16);
     const int kvrow = (DK == 128) ? row : (q4 * 16 + lane);
     const int dvt = p.dv_total;
-    const size_t sbase = static_cast<size_t>(bh) * DK * dvt;
     float kv[DVS];
+    // Segment start: the caller's initial state (or zero) at scan position 0, else the
+    // state the previous work range published for this unit.
+    auto load_state = [&](int bh, int slice, int pos) {
 #pragma unroll
-    for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
-    if (p.kv_in != nullptr && has_kv) {
-      const int c0 = slice * DVS;
-      if (!kv_in_T) {
-        const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * dvt + c0;
+      for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
+      if (pos == 0) {
+        if (p.kv_in != nullptr && has_kv) {
+          const size_t sbase = static_cast<size_t>(bh) * DK * dvt;
+          const int c0 = slice * DVS;
+          if (!kv_in_T) {
+            const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * dvt + c0;
 #pragma unroll
-        for (int j = 0; j < DVS; j += 4) {
-          float4 w = *reinterpret_cast<const float4*>(src + j);
-          kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
+            for (int j = 0; j < DVS; j += 4) {
+              float4 w = *reinterpret_cast<const float4*>(src + j);
+              kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
+            }
+          } else {
+            // state stored transposed: [dv_total][DK]
+#pragma unroll
+            for (int j = 0; j < DVS; ++j)
+              kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * DK + kvrow];
+          }
         }
       } else {
-        // state stored transposed: [dv_total][DK]
+        const int slot = (cid - 1) * CS + static_cast<int>(crank);
+        if (warp == W0 && lane == 0) flag_wait_consume(p.flags + slot);
+        named_bar_sync(5, 128);
+        if (has_kv) {
+          const float4* src = reinterpret_cast<const float4*>(
+              p.ws + (static_cast<size_t>(slot) * DK + kvrow) * DVS);
 #pragma unroll
-        for (int j = 0; j < DVS; ++j)
-          kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * DK + kvrow];
+          for (int j = 0; j < DVS; j += 4) {
+            float4 w = __ldcg(src + j / 4);
+            kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
+          }
+        }
       }
-    }
+    };
+    // Segment end: the caller's final state at the last scan position, else publish the
+    // state for the next work range (which continues this unit).
+    auto store_state = [&](int bh, int slice, int pos) {
+      if (pos == nblk - 1) {
+        if (kv_out != nullptr && has_kv) {
+          float* dst = kv_out + static_cast<size_t>(bh) * DK * dvt + static_cast<size_t>(kvrow) * dvt +
+                       slice * DVS;
+#pragma unroll
+          for (int j = 0; j < DVS; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
+        }
+      } else {
+        const int slot = cid * CS + static_cast<int>(crank);
+        if (has_kv) {
+          float4* dst = reinterpret_cast<float4*>(p.ws + (static_cast<size_t>(slot) * DK + kvrow) * DVS);
+#pragma unroll
+          for (int j = 0; j < DVS; j += 4) __stcg(dst + j / 4, make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]));
+        }
+        __threadfence();
+        named_bar_sync(5, 128);
+        if (warp == W0 && lane == 0) flag_release(p.flags + slot, 1);
+      }
+    };
     uint8_t* sKVb = smem + L::OFF_KV;
+    if (T > 0) {
+      mbar_wait(&bars[L::B_FULL + 0], 0);
+      const BlkRec rc = recs[0];
+      load_state(rc.bh, rc.slice, rc.pos);
+    }
     if (!SO) {
       if (has_kv) {
 #pragma unroll
@@ -468,15 +576,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
     }
-    for (int j = 0; j <= nblk; ++j) {
-      if (j < nblk) {
-        // ---- K~(j): scaled copy of the K rows
+    for (int j = 0; j <= T; ++j) {
+      if (j < T) {
+        // ---- K~(j): scaled copy of the V rows (the fold operand)
         const int s = j % NS, kt = j % KTS;
-        const int blk = REV ? (nblk - 1 - j) : j;
-        const int r = min(BT, N - blk * BT);
-        const float c = REV ? lam_pow(l2, row + 1) : (row < r ? lam_pow(l2, r - 1 - row) : 0.f);
         if (warp == W0) TR(3, j, 0);
         mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+        const BlkRec rc = recs[j & 7];
+        const int r = min(BT, N - rc.blk * BT);
+        const float c = REV ? lam_pow(rc.l2, row + 1) : (row < r ? lam_pow(rc.l2, r - 1 - row) : 0.f);
         if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
         if (warp == W0) TR(3, j, 1);
         scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
@@ -489,9 +597,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (j >= 1) {
         // ---- U(j-1): KV <- lam^r KV + dKV
         const int i = j - 1;
-        const int blk = REV ? (nblk - 1 - i) : i;
+        // record i was acquired in K~(i); its ring slot outlives U(i) (see the producer)
+        const BlkRec ru = recs[i & 7];
+        const int bh = ru.bh, slice = ru.slice, pos = ru.pos, blk = ru.blk, flags = ru.flags;
+        const float up_l2 = ru.l2;
         const int r = min(BT, N - blk * BT);
-        const float fr = lam_pow(l2, static_cast<float>(r));
+        const float fr = lam_pow(up_l2, static_cast<float>(r));
         if (warp == W0) TR(3, i, 3);
         const int db = i & 1;
         mbar_wait(&bars[L::B_DKVFULL + db], (i >> 1) & 1);
@@ -510,6 +621,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[L::B_DKVEMPTY + db]);
+        if (flags & REC_SEG_END) store_state(bh, slice, pos);
+        if (j < T) {
+          const BlkRec rn = recs[j & 7];  // acquired in K~(j) above
+          if (rn.flags & REC_SEG_START) load_state(rn.bh, rn.slice, rn.pos);
+        }
         if (!SO) {
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
           mbar_wait(&bars[L::B_OEFULL], i & 1);
@@ -523,12 +639,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (warp == W0) TR(3, i, 5);
       }
-    }
-    if (kv_out != nullptr && has_kv) {
-      float* dst = kv_out + sbase + static_cast<size_t>(kvrow) * dvt + slice * DVS;
-#pragma unroll
-      for (int j = 0; j < DVS; j += 4)
-        *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
     }
   }
   tc_fence_before();
@@ -571,6 +681,26 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r) - 1000;
 }
 
+// Tuning knobs (la2_set_tuning; defaults overridable by env for development).
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+static int g_persistent = env_int("LA2_NO_PERSIST", 0) ? 0 : 1;
+static int g_prefetch = env_int("LA2_PF", 1);
+static int g_l2hint = env_int("LA2_HINT", 3);
+static bool persistent_enabled() { return g_persistent != 0; }
+static int prefetch_blocks() { return g_prefetch; }
+static int l2_hints() { return g_l2hint; }
+int set_tuning(int key, int value) {
+  switch (key) {
+    case LA2_TUNE_PERSISTENT: g_persistent = value; return 0;
+    case LA2_TUNE_PREFETCH: g_prefetch = value; return 0;
+    case LA2_TUNE_L2HINT: g_l2hint = value; return 0;
+    default: return set_error(LA2_ERR_VALUE, "unknown tuning key");
+  }
+}
+
 template <int DK, bool REV, bool SO, int CM>
 static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullptr) {
   using L = TcLayout<DK, SO>;
@@ -606,18 +736,55 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
+  p.pf = prefetch_blocks();
+  p.hint = l2_hints();
+  // persistent schedule: units = independent recurrences (a cluster's pair counts once)
+  constexpr int CS = CM ? 2 : 1;
+  p.nsl = a.dv / DVS;
+  p.units = (CM == 2) ? BH : (CM == 1 ? BH * p.nsl / 2 : BH * p.nsl);
+  p.P = p.units;
+  p.ws = nullptr;
+  p.flags = nullptr;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CM == 2 ? 2 : a.dv / DVS, a.H, a.B);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CM ? 2 : 1;
+  attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CM ? 1 : 0;
+  if (persistent_enabled()) {
+    // co-resident work ranges (one CTA per SM: smem and TMEM are sized for it)
+    static int max_ranges = -1;
+    if (max_ranges < 0) {
+      int n = 0;
+      if (CM) {
+        cfg.gridDim = dim3(CS);
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+      } else {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, L::TOTAL) != cudaSuccess)
+          per_sm = 0;
+        n = sms * per_sm;
+      }
+      cudaGetLastError();
+      max_ranges = n;
+    }
+    if (max_ranges > 0 && p.units > max_ranges) {
+      const Workspace w = get_workspace(st);
+      if (w.ws != nullptr && w.slots >= max_ranges * CS) {
+        p.P = max_ranges;
+        p.ws = w.ws;
+        p.flags = w.flags;
+      }
+    }
+  }
+  cfg.gridDim = dim3(p.P * CS);
   e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mo1, p);
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   e = cudaGetLastError();

@@ -71,4 +71,132 @@ __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+// ------------------------------------------------------- persistent schedule
+// The flattened work space is units x nblk blocks (a unit = one (b, h, value slice)
+// recurrence, or a cluster's pair of them). P persistent CTAs (or clusters) each take
+// the contiguous range [c*W/P, (c+1)*W/P). When W/P >= nblk a range holds at most one
+// partial unit at each end, processed in this order:
+//   prefix  unit ub, blocks [0, ib)        first: from kv_in, publishes its end state
+//   full    units ufull0 .. ufull0+nfull-1 from kv_in to kv_out
+//   suffix  unit ua, blocks [ia, nblk)     last: starts from the state the previous
+//                                          range's prefix published
+// so a suffix only ever waits for work its neighbour did first (stream-K for the
+// sequential scan; no extra HBM traffic, only a d x 64 fp32 handoff per split unit).
+struct Sched {
+  int nblk, npre, upre, nfull, ufull0, usuf, isuf, T;
+  __device__ __forceinline__ void init(int c, int P, int units, int nblk_) {
+    nblk = nblk_;
+    const long long W = static_cast<long long>(units) * nblk;
+    const long long a = W * c / P, b = W * (c + 1) / P;
+    const int ua = static_cast<int>(a / nblk), ia = static_cast<int>(a % nblk);
+    const int ub = static_cast<int>(b / nblk), ib = static_cast<int>(b % nblk);
+    npre = ib;
+    upre = ub;
+    usuf = ua;
+    isuf = ia;
+    ufull0 = ia > 0 ? ua + 1 : ua;
+    nfull = ub - ufull0;
+    T = static_cast<int>(b - a);
+  }
+  // g-th block in processing order -> (unit, position i in the unit's scan order)
+  __device__ __forceinline__ void map(int g, int& u, int& i) const {
+    if (g < npre) {
+      u = upre;
+      i = g;
+      return;
+    }
+    g -= npre;
+    if (g < nfull * nblk) {
+      u = ufull0 + g / nblk;
+      i = g - (u - ufull0) * nblk;
+      return;
+    }
+    u = usuf;
+    i = isuf + (g - nfull * nblk);
+  }
+};
+
+// Sequential walk over a Sched range without per-block integer division (a division
+// chain costs ~100s of cycles and the walk sits on the critical path of the state and
+// row warps). Unit -> (b*H+h, value slice) is recomputed only when the unit changes.
+//   CM 0: unit = (bh, slice)   CM 1: unit = (bh, slice pair), slice = 2*pair + crank
+//   CM 2: unit = bh
+template <int CM>
+struct Walk {
+  int g, u, pos, bh, slice, h;
+  __device__ __forceinline__ void set_unit(int uu, int nsl, int H, int crank) {
+    u = uu;
+    if (CM == 0) {
+      bh = u / nsl;
+      slice = u - bh * nsl;
+    } else if (CM == 1) {
+      const int np = nsl >> 1;
+      bh = u / np;
+      slice = 2 * (u - bh * np) + crank;
+    } else {
+      bh = u;
+      slice = 0;
+    }
+    h = bh % H;
+  }
+  __device__ __forceinline__ void start(const Sched& s, int g0, int nsl, int H, int crank) {
+    g = g0;
+    int uu, pp;
+    s.map(g0 < s.T ? g0 : s.T - 1, uu, pp);
+    pos = pp;
+    set_unit(uu, nsl, H, crank);
+  }
+  __device__ __forceinline__ void next(const Sched& s, int nsl, int H, int crank) {
+    ++g;
+    ++pos;
+    if (g == s.npre) {  // prefix done -> first full unit, or the suffix
+      if (s.nfull > 0) {
+        pos = 0;
+        set_unit(s.ufull0, nsl, H, crank);
+      } else {
+        pos = s.isuf;
+        set_unit(s.usuf, nsl, H, crank);
+      }
+    } else if (pos == s.nblk && g < s.T) {  // a full unit done -> next full unit or suffix
+      if (u + 1 < s.ufull0 + s.nfull) {
+        pos = 0;
+        set_unit(u + 1, nsl, H, crank);
+      } else {
+        pos = s.isuf;
+        set_unit(s.usuf, nsl, H, crank);
+      }
+    }
+  }
+};
+
+// Per-block schedule record: written by the TMA producer (which walks the Sched range)
+// before the stage's FULL arrive, read by the row and state warps after their FULL wait,
+// so those warps carry no schedule state of their own.
+constexpr int REC_SEG_START = 1;  // first block of a segment: load kv_in / handoff
+constexpr int REC_SEG_END = 2;    // last block of a segment: store kv_out / handoff
+struct __align__(16) BlkRec {
+  int bh, slice, pos, blk;
+  float l2;  // log2(decay) of the head
+  int h, flags, pad;
+};
+
+__device__ __forceinline__ void flag_release(int* f, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(const int* f) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+// Wait for a handoff flag, then consume it (each flag has exactly one reader).
+// Bounded: a missing producer traps instead of hanging the GPU.
+__device__ __forceinline__ void flag_wait_consume(int* f) {
+  long long spins = 0;
+  while (flag_acquire(f) == 0) {
+    __nanosleep(64);
+    if (++spins > (1ll << 27)) __trap();
+  }
+  *reinterpret_cast<volatile int*>(f) = 0;
+}
+
 }  // namespace la2

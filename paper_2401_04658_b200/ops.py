@@ -209,6 +209,15 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     return dq, dk, dvv, dkv_out
 
 
+TUNE_PERSISTENT, TUNE_PREFETCH, TUNE_L2HINT = 1, 2, 3
+
+
+def set_tuning(key: int, value: int) -> None:
+    """Process-wide scheduling knob of the tensor-core kernels (include/la2.h
+    la2_set_tuning). Outputs do not depend on it."""
+    _lib.call("la2_set_tuning", int(key), int(value))
+
+
 def chunk_state(k, v, decay: DecayLike) -> torch.Tensor:
     """S = sum_s lam^(N-1-s) k_s^T v_s  (fp32 [B,H,d,dv]); sequence-parallel pass A."""
     B, H, N, d, dv = _check_qkv(k, k, v)

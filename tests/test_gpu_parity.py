@@ -388,3 +388,43 @@ def test_autograd_auto_split():
     errs = {"o": rel(o, ro), "o_nosplit": rel(o1, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk),
             "dv": rel(vg.grad, rv)}
     assert max(errs.values()) <= BF16_TOL, errs
+
+
+# ------------------------------------------------------- persistent schedule
+@pytest.mark.parametrize("B,H,N,d,dv", [
+    (1, 160, 300, 64, 64),     # forward/dQ: one CTA per SM over 160 recurrences (no cluster)
+    (2, 45, 1000, 128, 128),   # value-slice pairs: 90 cluster units > co-resident clusters
+    (1, 200, 129, 64, 64),     # 2-block sequences: most ranges split a recurrence
+])
+def test_persistent_schedule_bitwise(B, H, N, d, dv):
+    """More recurrences than co-resident CTAs: the persistent schedule splits some
+    recurrences between neighbouring work ranges and hands the fp32 state over, so
+    every output (o, states, dq, dk, dv, chunk states) is bitwise identical to one CTA
+    per recurrence, and matches the oracle."""
+    q, k, v, do = inputs(B, H, N, d, dv, torch.bfloat16, seed=H + N)
+    decay = list(np.linspace(0.9, 1.0, H))
+    g = torch.Generator().manual_seed(3)
+    kv_in = (torch.rand(B, H, d, dv, generator=g) - 0.5).to(DEV)
+    dkv_in = (torch.rand(B, H, d, dv, generator=g) - 0.5).to(DEV)
+    qg, kg, vg, dog = gpu(q, k, v, do)
+
+    def run():
+        o, kv = la2.la2_forward(qg, kg, vg, decay, kv_in=kv_in, output_final_state=True)
+        grads = la2.la2_backward(qg, kg, vg, dog, decay, kv_in=kv_in, dkv_in=dkv_in, output_dkv=True)
+        s = la2.chunk_state(kg, vg, decay)
+        t = la2.chunk_dstate(qg, dog, decay)
+        torch.cuda.synchronize()
+        return [o, kv, *grads, s, t]
+
+    try:
+        la2.set_tuning(la2.ops.TUNE_PERSISTENT, 1)
+        a = run()
+        la2.set_tuning(la2.ops.TUNE_PERSISTENT, 0)
+        b = run()
+    finally:
+        la2.set_tuning(la2.ops.TUNE_PERSISTENT, 1)
+    names = ["o", "kv", "dq", "dk", "dv", "dkv", "S", "T"]
+    for n, x, y in zip(names, a, b):
+        assert torch.equal(x, y), f"{n} differs between persistent and one-CTA-per-recurrence"
+    ro, rkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay, kv_in=to64(kv_in))
+    assert max(rel(a[0], ro), rel(a[1], rkv)) <= BF16_TOL

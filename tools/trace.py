@@ -1,6 +1,6 @@
 """Phase trace of CTA (0,0,0) of one forward F launch (needs libla2_trace.so)."""
 import ctypes, os, sys
-os.environ['LA2_LIB'] = os.path.join(os.path.dirname(__file__), '..', 'paper_2401_04658_b200', 'libla2_trace.so')
+os.environ.setdefault('LA2_LIB', os.path.join(os.path.dirname(__file__), '..', 'paper_2401_04658_b200', 'libla2_trace.so'))
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2401_04658_b200 as la2
