@@ -442,22 +442,32 @@ def extra_workload(args, world, rank, local_rank):
                                 "api": "lightning_attn2 autograd"},
                      "per_dtype": results})
         if w == "c4":
-            Bd, steps_d = 64, 256
-            st0 = torch.zeros(Bd, H, D, D, device=dev)
-            qd, kd, vd = (rand((steps_d, Bd, H, D), torch.bfloat16, 10 + i) for i in range(3))
-            st = st0.clone()
-            la2.decode_step(qd[0], kd[0], vd[0], dec, st)  # warm the launch path
-            graph = torch.cuda.CUDAGraph()
-            st.copy_(st0)
-            with torch.cuda.graph(graph):
-                for t in range(steps_d):
-                    la2.decode_step(qd[t], kd[t], vd[t], dec, st)
-            ms_d = timed(graph.replay, max(3, args.steps // 4), 2)
-            state_bytes = Bd * H * D * D * 4 * 2
-            line["decode"] = {"batch": Bd, "steps_per_graph": steps_d, "ms_per_graph": ms_d,
-                              "tokens_per_s": Bd * steps_d * world / (ms_d / 1e3),
-                              "state_gbs": state_bytes * steps_d / (ms_d / 1e3) / 1e9,
-                              "frac_of_hbm": state_bytes * steps_d / (ms_d / 1e3) / 1e9 / hbm_peak}
+            # Recurrent decode (tila.inference_step): one launch per token, graph-captured.
+            # Batch 64 keeps the fp32 state (84 MB) L2-resident across steps; batch 256
+            # (336 MB) streams it from HBM every step, which is the bandwidth-bound case.
+            line["decode"] = []
+            for Bd in (64, 256):
+                steps_d = 256 if Bd == 64 else 64
+                st0 = torch.zeros(Bd, H, D, D, device=dev)
+                qd, kd, vd = (rand((steps_d, Bd, H, D), torch.bfloat16, 10 + i) for i in range(3))
+                st = st0.clone()
+                la2.decode_step(qd[0], kd[0], vd[0], dec, st)  # warm the launch path
+                graph = torch.cuda.CUDAGraph()
+                st.copy_(st0)
+                with torch.cuda.graph(graph):
+                    for t in range(steps_d):
+                        la2.decode_step(qd[t], kd[t], vd[t], dec, st)
+                ms_d = timed(graph.replay, max(3, args.steps // 4), 2)
+                state_bytes = Bd * H * D * D * 4 * 2  # fp32 state read + write per step
+                gbs = state_bytes * steps_d / (ms_d / 1e3) / 1e9
+                line["decode"].append({
+                    "batch": Bd, "steps_per_graph": steps_d, "ms_per_graph": ms_d,
+                    "us_per_step": ms_d * 1e3 / steps_d,
+                    "tokens_per_s": Bd * steps_d * world / (ms_d / 1e3), "state_gbs": gbs,
+                    "state_mb": Bd * H * D * D * 4 / 2**20,
+                    "residency": "L2" if Bd * H * D * D * 4 < 100 * 2**20 else "HBM",
+                    "frac_of_hbm": gbs / hbm_peak})
+                del st0, st, qd, kd, vd, graph
     else:  # c5
         H, D, N_total = 16, 128, 524288
         L = N_total // world

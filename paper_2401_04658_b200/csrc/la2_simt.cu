@@ -224,9 +224,96 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Bandwidth-shaped decode for d * dv a multiple of 1024 and dv / 4 dividing 256: each of
+// the 256 threads owns PER float4 of the fp32 state (fixed 4 value columns, rows strided
+// by 256 / (dv / 4)), issues all its state loads before any arithmetic (PER x 16 bytes
+// in flight per thread), writes the updated state back and reduces o over rows in smem.
+template <typename T, int PER>
+__global__ void __launch_bounds__(256)
+    la2_decode_vec_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                          const float* __restrict__ decay, float* __restrict__ state,
+                          T* __restrict__ o, int H, int d, int dv) {
+  __shared__ float qs[256], ks[256];
+  __shared__ float4 red[256];
+  const int bh = blockIdx.x, t = threadIdx.x;
+  const float lam = decay[bh % H];
+  if (t < d) {
+    qs[t] = ld_el<T>(q + static_cast<size_t>(bh) * d + t);
+    ks[t] = ld_el<T>(k + static_cast<size_t>(bh) * d + t);
+  }
+  const int C4 = dv >> 2, R = 256 / C4;
+  const int c4 = t % C4, r0 = t / C4;
+  float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv);
+  float4 x[PER];
+#pragma unroll
+  for (int m = 0; m < PER; ++m) x[m] = S[(r0 + m * R) * C4 + c4];
+  float4 vv;
+  vv.x = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4);
+  vv.y = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 1);
+  vv.z = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 2);
+  vv.w = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 3);
+  __syncthreads();
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const int i = r0 + m * R;
+    const float ki = ks[i], qi = qs[i];
+    float4 y;
+    y.x = fmaf(lam, x[m].x, ki * vv.x);
+    y.y = fmaf(lam, x[m].y, ki * vv.y);
+    y.z = fmaf(lam, x[m].z, ki * vv.z);
+    y.w = fmaf(lam, x[m].w, ki * vv.w);
+    S[i * C4 + c4] = y;
+    acc.x = fmaf(qi, y.x, acc.x);
+    acc.y = fmaf(qi, y.y, acc.y);
+    acc.z = fmaf(qi, y.z, acc.z);
+    acc.w = fmaf(qi, y.w, acc.w);
+  }
+  red[t] = acc;
+  __syncthreads();
+  if (t < C4) {
+    float4 s = red[t];
+    for (int r = 1; r < R; ++r) {
+      const float4 w = red[r * C4 + t];
+      s.x += w.x; s.y += w.y; s.z += w.z; s.w += w.w;
+    }
+    T* op = o + static_cast<size_t>(bh) * dv + 4 * t;
+    st_el<T>(op, s.x);
+    st_el<T>(op + 1, s.y);
+    st_el<T>(op + 2, s.z);
+    st_el<T>(op + 3, s.w);
+  }
+}
+
+template <typename T>
+static bool launch_decode_vec(const void* q, const void* k, const void* v, const float* decay,
+                              float* state, void* o, int B, int H, int d, int dv, cudaStream_t st) {
+  if (dv % 4 || 256 % (dv / 4) || (d * dv) % 1024 || d > 256) return false;
+  const int per = d * dv / 1024;
+  const T* tq = static_cast<const T*>(q);
+  const T* tk = static_cast<const T*>(k);
+  const T* tv = static_cast<const T*>(v);
+  T* to = static_cast<T*>(o);
+  switch (per) {
+#define LA2_DEC(P) \
+  case P: la2_decode_vec_kernel<T, P><<<B * H, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv); return true;
+    LA2_DEC(1) LA2_DEC(2) LA2_DEC(4) LA2_DEC(8) LA2_DEC(16) LA2_DEC(32)
+#undef LA2_DEC
+    default: return false;
+  }
+}
+
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st) {
   if (dv > 256) return set_error(LA2_ERR_UNSUPPORTED, "decode supports dv <= 256");
+  const bool vec = (dtype == LA2_FP32)
+                       ? launch_decode_vec<float>(q, k, v, decay, state, o, B, H, d, dv, st)
+                       : launch_decode_vec<__nv_bfloat16>(q, k, v, decay, state, o, B, H, d, dv, st);
+  if (vec) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error("la2_decode_vec_kernel launch", e);
+    return 0;
+  }
   const size_t smem = sizeof(float) * (2 * d + dv + 256);
   const int threads = (256 / dv) * dv;
   if (dtype == LA2_FP32)
