@@ -160,6 +160,12 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
     FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
     return launch_tc_pair(av, ak, st);
   }
+  if (dtype == LA2_BF16 && d == 128 && dvd == 128) {
+    // dV and dK scans as one 4-CTA cluster per unit (sweep 2, kernel.py:207-231)
+    FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
+    FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+    return launch_tc_quad(av, ak, st);
+  }
   // dK = F_rev(V, dO, Q): reverse scan, state dKV^T  (sweep 2, kernel.py:207-216)
   FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
   if (int rc = run_f(ak, st)) return rc;

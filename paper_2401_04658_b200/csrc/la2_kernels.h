@@ -44,6 +44,8 @@ struct FParams {
 int launch_tc(const FArgs& a, cudaStream_t st);
 // dV and dK reverse scans as one 2-CTA cluster per head (shared Q / dO tiles).
 int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st);
+// d = dv = 128: dV and dK reverse scans as one 4-CTA cluster per unit (two value-slice pairs).
+int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 // Fused reverse scan of the backward pass (dK and dV together), d = dv = 64, bf16.
 int launch_g(const void* q, const void* k, const void* v, const void* dout, void* dk, void* dv,
              const float* decay, const float* dkv_in, float* dkv_out, int B, int H, int N,

@@ -62,14 +62,19 @@ struct TcLayout {
   static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
   static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
-  // TMEM columns: S[2] @0,128 (P aliased) | O @256 | Oe @320 | dKV[2] @384,448
-  // (state-only: dKV[2] @0,64)
+  // TMEM columns. OIS ("O in S", d = 128): S[b] @128b holds the scores, then P (packed
+  // bf16, cols +0..63) and O_i = P_i V_i (fp32, cols +64..127), so O is double-buffered
+  // with S and PV_i does not wait for the epilogue of block i-1 | Oe[2] @256,320 |
+  // dKV[2] @384,448. Otherwise (d = 64): S[2] @0,128 (P in cols +0..31, +64..95) | O @256
+  // | Oe @320 | dKV[2] @384,448 -- S_{i+2} then only waits for PV_i, not for the epilogue.
+  // State-only: dKV[2] @0,64.
+  static constexpr bool OIS = (DK == 128);
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
-  static constexpr uint32_t T_O = 256, T_OE = 320, T_KV = SO ? 0 : 384;
+  static constexpr uint32_t T_O = 256, T_OE = OIS ? 256 : 320, T_KV = SO ? 0 : 384;
   // barrier slots
   static constexpr int B_FULL = 0, B_EMPTY = NS, B_SFULL = 2 * NS, B_SFREE = B_SFULL + 2,
-                       B_PREADY = B_SFREE + 2, B_OFULLX = B_PREADY + 2, B_OEFULL = B_OFULLX + 1,
-                       B_OEMPTY = B_OEFULL + 1, B_KTREADY = B_OEMPTY + 1, B_KTFREE = B_KTREADY + KTS,
+                       B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEFULL = B_OFULL + 2,
+                       B_OEMPTY = B_OEFULL + 2, B_KTREADY = B_OEMPTY + 2, B_KTFREE = B_KTREADY + KTS,
                        B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 2,
                        B_KVREADY = B_DKVEMPTY + 2, B_COUNT = B_KVREADY + 1;
   static_assert(B_COUNT * 8 + 16 <= BAR_BYTES, "barrier area");
@@ -88,12 +93,14 @@ template <int DK, bool REV, bool SO, int CM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     la2_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                  const __grid_constant__ CUtensorMap tm_q1, const __grid_constant__ CUtensorMap tm_o1,
+                  const __grid_constant__ CUtensorMap tm_q1, const __grid_constant__ CUtensorMap tm_k1,
+                  const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_o1,
                   const FParams p) {
   using L = TcLayout<DK, SO>;
   constexpr bool CL = (CM != 0);
-  constexpr int CS = CL ? 2 : 1;  // CTAs per cluster
+  constexpr int CS = (CM == 3) ? 4 : (CL ? 2 : 1);  // CTAs per cluster
   static_assert(CM != 2 || (DK == 64 && REV && !SO), "backward pair needs d = dv = 64");
+  static_assert(CM != 3 || (DK == 128 && REV && !SO), "backward quad needs d = dv = 128");
   static_assert(!(CL && SO), "state-only passes run without clusters");
   constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
   extern __shared__ uint8_t smem_raw[];
@@ -105,11 +112,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = CL ? cluster_ctarank() : 0;
-  const bool sib = (CM == 2) && (crank == 1);      // sibling pass of the backward pair
+  // CM 3: ranks 0-1 run one pass (value-slice pair), ranks 2-3 the sibling pass
+  const int pair = (CM == 3) ? static_cast<int>(crank >> 1) : 0;
+  const uint32_t prank = (CM == 3) ? (crank & 1) : crank;    // rank inside the pair
+  const uint16_t mcmask = static_cast<uint16_t>(0x3u << (2 * pair));  // this pair's CTAs
+  const bool sib = ((CM == 2) && (crank == 1)) || ((CM == 3) && pair == 1);  // sibling pass
   const CUtensorMap* mq = sib ? &tm_q1 : &tm_q;
   const CUtensorMap* mo = sib ? &tm_o1 : &tm_o;
-  const int offk = sib ? L::OFF_V : L::OFF_K;       // this CTA's k tile region
-  const int offv = sib ? L::OFF_K : L::OFF_V;       // this CTA's v tile region
+  const CUtensorMap* mk = (CM == 3 && sib) ? &tm_k1 : &tm_k;
+  const CUtensorMap* mv = (CM == 3 && sib) ? &tm_v1 : &tm_v;
+  const int offk = (CM == 2 && sib) ? L::OFF_V : L::OFF_K;  // this CTA's k tile region
+  const int offv = (CM == 2 && sib) ? L::OFF_K : L::OFF_V;  // this CTA's v tile region
   const int kv_in_T = sib ? 1 : p.kv_in_T;          // the dK pass carries dKV^T
   float* const kv_out = sib ? nullptr : p.kv_out;
   const int N = p.N;
@@ -118,7 +131,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   Sched sch;
   sch.init(cid, p.P, p.units, nblk);
   const int T = sch.T;
-  const int nsl = p.nsl, H = p.H, cr = static_cast<int>(crank);
+  const int nsl = p.nsl, H = p.H, cr = static_cast<int>(prank);
   auto blk_of = [&](int pos) { return REV ? (nblk - 1 - pos) : pos; };
   // exact log2 of the head's decay (fast-math log2f is off by ~2^-22 absolute, which
   // compounds over 64K tokens when lam is close to 1)
@@ -135,12 +148,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[L::B_SFULL + b], 1);
-      mbar_init(&bars[L::B_SFREE + b], 1);
+      mbar_init(&bars[L::B_SFREE + b], L::OIS ? NROW : 1);  // OIS: B(i) read O_i out of S[b]
       mbar_init(&bars[L::B_PREADY + b], NROW);
+      mbar_init(&bars[L::B_OFULL + b], 1);
+      mbar_init(&bars[L::B_OEFULL + b], 1);
+      mbar_init(&bars[L::B_OEMPTY + b], NROW);
     }
-    mbar_init(&bars[L::B_OFULLX], 1);
-    mbar_init(&bars[L::B_OEFULL], 1);
-    mbar_init(&bars[L::B_OEMPTY], NROW);
     for (int b = 0; b < KTS; ++b) {
       mbar_init(&bars[L::B_KTREADY + b], 4);
       mbar_init(&bars[L::B_KTFREE + b], 1);
@@ -154,8 +167,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   if (warp == 0 && lane == 0) {
     if (!SO) tma_prefetch_desc(mq);
-    tma_prefetch_desc(&tm_k);
-    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(mk);
+    tma_prefetch_desc(mv);
     if (!SO) tma_prefetch_desc(mo);
   }
   if (warp == 1) tmem_alloc(tmem_slot, L::TMEM_COLS);
@@ -198,10 +211,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_prefetch_l2_3d(&tm_k, c * 64, b2 * BT, bh);
           }
           tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
-        } else if (CM == 1) {
+        } else if (CM == 1 || CM == 3) {
 #pragma unroll
-          for (int c = 0; c < DK / 64; ++c) tma_prefetch_l2_3d(crank ? &tm_k : &tm_q, c * 64, b2 * BT, bh);
-          tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
+          for (int c = 0; c < DK / 64; ++c) tma_prefetch_l2_3d(prank ? mk : mq, c * 64, b2 * BT, bh);
+          tma_prefetch_l2_3d(mv, slice * DVS, b2 * BT, bh);
         } else {
           tma_prefetch_l2_3d(mq, 0, b2 * BT, bh);
           tma_prefetch_l2_3d(crank ? &tm_v : &tm_k, 0, b2 * BT, bh);
@@ -251,13 +264,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_load_3d(dk + c * REGION, &tm_k, fb, c * 64, row, bh);
           }
           tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
-        } else if (CM == 1) {
+        } else if (CM == 1 || CM == 3) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
-            if (crank == 0) tma_load_3d_mc(dq + c * REGION, &tm_q, fb, c * 64, row, bh, 0x3);
-            else tma_load_3d_mc(dk + c * REGION, &tm_k, fb, c * 64, row, bh, 0x3);
+            if (prank == 0) tma_load_3d_mc(dq + c * REGION, mq, fb, c * 64, row, bh, mcmask);
+            else tma_load_3d_mc(dk + c * REGION, mk, fb, c * 64, row, bh, mcmask);
           }
-          tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
+          tma_load_3d(dv, mv, fb, slice * DVS, row, bh);
         } else {
           tma_load_3d(dq, mq, fb, 0, row, bh);  // own q: K (rank 0) or V (rank 1)
           if (crank == 0) tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K
@@ -277,13 +290,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr uint32_t ID_O = idesc_bf16(128, DVS, 0, 1);  // P/Q (K-major) x V/KV (MN-major)
     constexpr uint32_t ID_KV = idesc_bf16(DK, DVS, 1, 1);  // K~^T (MN-major) x V (MN-major)
     const bool leader = (lane == 0);
-    const uint32_t tO = tbase + L::T_O, tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
+    const uint32_t tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
     // descriptor bases (start address is in 16-byte units in the low bits)
     const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
     const uint64_t dK0 = sdesc_sw128(smem_u32(smem + offk), 16, 1024);
     const uint64_t dV0 = sdesc_sw128(smem_u32(smem + offv), REGION, 1024);
     auto commit_empty = [&](int s) {
-      if (CL) umma_commit_mc(&bars[L::B_EMPTY + s], 0x3);
+      if (CL) umma_commit_mc(&bars[L::B_EMPTY + s], mcmask);
       else umma_commit(&bars[L::B_EMPTY + s]);
     };
     const uint64_t dKT0 = sdesc_sw128(smem_u32(smem + L::OFF_KT), REGION, 1024);
@@ -291,8 +304,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     auto adv = [](uint64_t d, uint32_t bytes) { return d + static_cast<uint64_t>(bytes >> 4); };
 
     if (warp == 1) {
-      // ---- X: score chain  S_{i+1} = Q K^T ; O_i = P_i V_i
-      if (!SO) {
+      // ---- X: score chain  S_j = Q K^T ; O_i = P_i V_i
+      // Event loop: S_j (needs stage j loaded and S buffer j&1 free) and PV_i (needs P_i
+      // and the O accumulator free) are issued as soon as each is ready, so PV_i never
+      // waits behind the arrival of block i+1 -- that coupling would keep only one stage
+      // load in flight with a 2-stage ring. S runs at most one block ahead of PV.
+      if (!SO && NS >= 3) {
+        // deep ring (d = 64): block i+1 has normally landed before PV_i is due, so the
+        // plain order S_{i+1}, PV_i keeps the tensor pipe fed with the least polling
         auto issue_S = [&](int j) {
           const int s = j % NS, b = j & 1;
           mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
@@ -313,22 +332,72 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int i = 0; i < T; ++i) {
           const int s = i % NS, b = i & 1;
           const uint64_t v = adv(dV0, s * L::V_BYTES);
-          TR(1, i, 0);
           if (i + 1 < T) issue_S(i + 1);
-          TR(1, i, 1);
           mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
-          TR(1, i, 2);
-          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
-          TR(1, i, 3);
+          if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           tc_fence_after();
           if (leader) {
 #pragma unroll
-            for (int kk = 0; kk < BT / 16; ++kk)
-              umma_bf16_ts(tO, tbase + b * 128 + (kk >> 2) * 64 + (kk & 3) * 8, adv(v, kk * 2048),
-                           ID_O, kk > 0);
-            umma_commit(&bars[L::B_SFREE + b]);
-            umma_commit(&bars[L::B_OFULLX]);
+            for (int kk = 0; kk < BT / 16; ++kk) {
+              const uint32_t pcol = L::OIS ? kk * 8 : (kk >> 2) * 64 + (kk & 3) * 8;
+              umma_bf16_ts(L::OIS ? tbase + b * 128 + 64 : tbase + L::T_O, tbase + b * 128 + pcol,
+                           adv(v, kk * 2048), ID_O, kk > 0);
+            }
+            if (!L::OIS) umma_commit(&bars[L::B_SFREE + b]);
+            umma_commit(&bars[L::B_OFULL + b]);
             commit_empty(s);
+          }
+          __syncwarp();
+        }
+      } else if (!SO) {
+        int nS = 0, nP = 0;
+        while (nP < T) {
+          bool s_ok = false, p_ok = false;
+          if (lane == 0) {
+            if (nS < T && nS <= nP + 1)
+              s_ok = mbar_test(&bars[L::B_FULL + nS % NS], (nS / NS) & 1) &&
+                     (nS < 2 || mbar_test(&bars[L::B_SFREE + (nS & 1)], ((nS >> 1) - 1) & 1));
+            if (nP < nS)
+              p_ok = mbar_test(&bars[L::B_PREADY + (nP & 1)], (nP >> 1) & 1) &&
+                     (L::OIS || nP == 0 || mbar_test(&bars[L::B_OEMPTY + ((nP - 1) & 1)], ((nP - 1) >> 1) & 1));
+          }
+          s_ok = __shfl_sync(0xffffffffu, s_ok, 0);
+          p_ok = __shfl_sync(0xffffffffu, p_ok, 0);
+          if (!s_ok && !p_ok) {
+            __nanosleep(32);
+            continue;
+          }
+          tc_fence_after();
+          if (s_ok) {
+            const int s = nS % NS, b = nS & 1;
+            TR(1, nS, 1);
+            if (leader) {
+              const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < DK / 16; ++kk) {
+                const uint32_t off = (kk >> 2) * REGION + (kk & 3) * 32;
+                umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
+              }
+              umma_commit(&bars[L::B_SFULL + b]);
+            }
+            ++nS;
+          }
+          if (p_ok) {
+            const int s = nP % NS, b = nP & 1;
+            const uint64_t v = adv(dV0, s * L::V_BYTES);
+            TR(1, nP, 3);
+            if (leader) {
+#pragma unroll
+              for (int kk = 0; kk < BT / 16; ++kk) {
+                const uint32_t pcol = L::OIS ? kk * 8 : (kk >> 2) * 64 + (kk & 3) * 8;
+                umma_bf16_ts(L::OIS ? tbase + b * 128 + 64 : tbase + L::T_O, tbase + b * 128 + pcol,
+                             adv(v, kk * 2048), ID_O, kk > 0);
+              }
+              if (!L::OIS) umma_commit(&bars[L::B_SFREE + b]);
+              umma_commit(&bars[L::B_OFULL + b]);
+              commit_empty(s);
+            }
+            ++nP;
           }
           __syncwarp();
         }
@@ -356,16 +425,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (!SO) {
           mbar_wait(&bars[L::B_KVREADY], i & 1);
-          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY], (i - 1) & 1);
+          if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
+          if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           TR(1, i, 4);
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES);
 #pragma unroll
             for (int kk = 0; kk < DK / 16; ++kk)
-              umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dKV0, kk * 2048),
-                           ID_O, kk > 0);
-            umma_commit(&bars[L::B_OEFULL]);
+              umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
+                           adv(dKV0, kk * 2048), ID_O, kk > 0);
+            umma_commit(&bars[L::B_OEFULL + db]);
             commit_empty(s);
           }
           __syncwarp();
@@ -418,21 +488,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&bars[L::B_SFULL + b], (j >> 1) & 1);
           if (warp == 2) TR(2, j, 1);
           tc_fence_after();
+          // 64 score columns -> 32 packed P columns at [32h, 32h+32): P ends up contiguous
+          // in columns 0..63 of S[b] and columns 64..127 are free for O_i = P_i V_i. The
+          // quarter's two warps sync between reading and writing (half 1 writes over
+          // score columns half 0 reads).
+          uint32_t pk[2][16];
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {  // 32 score columns -> 16 packed columns
+          for (int hh = 0; hh < 2; ++hh) {
             uint32_t raw[32];
             tmem_ld32_raw(tS + hh * 32, raw);
             tmem_ld_wait();
-            uint32_t pk[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int c = 2 * hh + (e >> 3), ch = 4 * half + c, jj = (2 * e) & 15;
               const float m0 = (ch == dch) ? Dg[jj] : F[c] * G[jj];
               const float m1 = (ch == dch) ? Dg[jj + 1] : F[c] * G[jj + 1];
-              pk[e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * m0,
-                                  __uint_as_float(raw[2 * e + 1]) * m1);
+              pk[hh][e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * m0,
+                                      __uint_as_float(raw[2 * e + 1]) * m1);
             }
-            tmem_st16(tS + hh * 16, pk);
+            if (!L::OIS) tmem_st16(tS + hh * 16, pk[hh]);  // in place: no cross-warp hazard
+          }
+          if (L::OIS) {
+            named_bar_sync(1 + q4, 64);
+            const uint32_t tP = tbase + b * 128 + half * 32 + lane_off;
+            tmem_st16(tP, pk[0]);
+            tmem_st16(tP + 16, pk[1]);
           }
           tmem_st_wait();
           tc_fence_before();
@@ -455,20 +535,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (storer) tma_store_wait_read<OS - 1>();
           named_bar_sync(1 + q4, 64);  // the two warps of this quarter
           if (warp == 2) TR(2, i, 4);
-          mbar_wait(&bars[L::B_OFULLX], i & 1);
-          mbar_wait(&bars[L::B_OEFULL], i & 1);
+          const int ob = i & 1;
+          mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
+          mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
           if (warp == 2) TR(2, i, 5);
           tc_fence_after();
           float o16[2][16], e16[2][16];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            tmem_ld16(tbase + L::T_O + lane_off + half * 32 + q * 16, o16[q]);
-            tmem_ld16(tbase + L::T_OE + lane_off + half * 32 + q * 16, e16[q]);
+            tmem_ld16((L::OIS ? tbase + ob * 128 + 64 : tbase + L::T_O) + lane_off + half * 32 + q * 16,
+                      o16[q]);
+            tmem_ld16(tbase + L::T_OE + (L::OIS ? ob * 64 : 0) + lane_off + half * 32 + q * 16, e16[q]);
           }
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[L::B_OEMPTY]);
+          if (lane == 0) {
+            if (L::OIS) mbar_arrive(&bars[L::B_SFREE + ob]);
+            mbar_arrive(&bars[L::B_OEMPTY + ob]);
+          }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -628,7 +713,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (!SO) {
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
-          mbar_wait(&bars[L::B_OEFULL], i & 1);
+          mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (has_kv) {
 #pragma unroll
             for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
@@ -687,9 +772,11 @@ static int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 static int g_persistent = env_int("LA2_NO_PERSIST", 0) ? 0 : 1;
-static int g_prefetch = env_int("LA2_PF", 1);
-static int g_l2hint = env_int("LA2_HINT", 3);
+static int g_prefetch = env_int("LA2_PF", 0);
+static int g_l2hint = env_int("LA2_HINT", 0);
+static int g_quad = env_int("LA2_NO_QUAD", 0) ? 0 : 1;
 static bool persistent_enabled() { return g_persistent != 0; }
+static bool quad_enabled() { return g_quad != 0; }
 static int prefetch_blocks() { return g_prefetch; }
 static int l2_hints() { return g_l2hint; }
 int set_tuning(int key, int value) {
@@ -697,6 +784,7 @@ int set_tuning(int key, int value) {
     case LA2_TUNE_PERSISTENT: g_persistent = value; return 0;
     case LA2_TUNE_PREFETCH: g_prefetch = value; return 0;
     case LA2_TUNE_L2HINT: g_l2hint = value; return 0;
+    case LA2_TUNE_FUSED_BWD: g_quad = value; return 0;
     default: return set_error(LA2_ERR_VALUE, "unknown tuning key");
   }
 }
@@ -711,14 +799,17 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     (void)e;
   }
-  CUtensorMap mq, mk, mv, mo, mq1, mo1;
+  // maps: q k v o of the pass, and of the sibling pass (CM 2: q1/o1 only; CM 3: all four)
+  CUtensorMap mq, mk, mv, mo, mq1, mk1, mv1, mo1;
   const int BH = a.B * a.H;
-  const void* ptrs[6] = {a.q, a.k, a.v, a.o, a1 ? a1->q : a.q, a1 ? a1->o : a.o};
-  CUtensorMap* maps[6] = {&mq, &mk, &mv, &mo, &mq1, &mo1};
-  const int cols[6] = {DK, DK, a.dv, a.dv, DK, a.dv};
-  for (int t = 0; t < 6; ++t) {
-    if (SO && (t == 0 || t == 3 || t == 4 || t == 5)) continue;
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 5) ? 32 : BT);
+  const void* ptrs[8] = {a.q, a.k, a.v, a.o, a1 ? a1->q : a.q, a1 ? a1->k : a.k,
+                         a1 ? a1->v : a.v, a1 ? a1->o : a.o};
+  CUtensorMap* maps[8] = {&mq, &mk, &mv, &mo, &mq1, &mk1, &mv1, &mo1};
+  const int cols[8] = {DK, DK, a.dv, a.dv, DK, DK, a.dv, a.dv};
+  for (int t = 0; t < 8; ++t) {
+    if (SO && t != 1 && t != 2) continue;
+    if (CM != 3 && (t == 5 || t == 6)) continue;
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),
@@ -728,6 +819,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     }
   }
   if (SO) { mq = mk; mo = mv; mq1 = mk; mo1 = mv; }
+  if (CM != 3) { mk1 = mk; mv1 = mv; }
   FParams p;
   p.N = a.N;
   p.H = a.H;
@@ -739,9 +831,9 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.pf = prefetch_blocks();
   p.hint = l2_hints();
   // persistent schedule: units = independent recurrences (a cluster's pair counts once)
-  constexpr int CS = CM ? 2 : 1;
+  constexpr int CS = (CM == 3) ? 4 : (CM ? 2 : 1);
   p.nsl = a.dv / DVS;
-  p.units = (CM == 2) ? BH : (CM == 1 ? BH * p.nsl / 2 : BH * p.nsl);
+  p.units = (CM == 2) ? BH : ((CM == 1 || CM == 3) ? BH * p.nsl / 2 : BH * p.nsl);
   p.P = p.units;
   p.ws = nullptr;
   p.flags = nullptr;
@@ -785,7 +877,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     }
   }
   cfg.gridDim = dim3(p.P * CS);
-  e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mo1, p);
+  e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mk1, mv1, mo1, p);
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
@@ -835,6 +927,18 @@ int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
     return launch_tc_t<64, true, false, 0>(adv, st);
   }
   return launch_tc_t<64, true, false, 2>(adv, st, &adk);
+}
+
+// d = dv = 128: the dV and dK reverse scans as one 4-CTA cluster per unit -- each pass
+// a value-slice pair (Q/K multicast inside the pair) -- so the Q and dO tiles both
+// passes read are fetched from HBM once and hit L2 for the second pass.
+int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
+  if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
+  if (!clusters_enabled() || !quad_enabled()) {
+    if (int rc = launch_tc(adk, st)) return rc;
+    return launch_tc(adv, st);
+  }
+  return launch_tc_t<128, true, false, 3>(adv, st, &adk);
 }
 
 }  // namespace la2

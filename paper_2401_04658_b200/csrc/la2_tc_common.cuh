@@ -120,7 +120,7 @@ struct Sched {
 // chain costs ~100s of cycles and the walk sits on the critical path of the state and
 // row warps). Unit -> (b*H+h, value slice) is recomputed only when the unit changes.
 //   CM 0: unit = (bh, slice)   CM 1: unit = (bh, slice pair), slice = 2*pair + crank
-//   CM 2: unit = bh
+//   CM 2: unit = bh      CM 3: as CM 1 (each pass's pair walks the same units)
 template <int CM>
 struct Walk {
   int g, u, pos, bh, slice, h;
@@ -129,7 +129,7 @@ struct Walk {
     if (CM == 0) {
       bh = u / nsl;
       slice = u - bh * nsl;
-    } else if (CM == 1) {
+    } else if (CM == 1 || CM == 3) {
       const int np = nsl >> 1;
       bh = u / np;
       slice = 2 * (u - bh * np) + crank;

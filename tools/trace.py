@@ -8,7 +8,8 @@ from paper_2401_04658_b200 import _lib
 from bench import alibi_decay
 lib = _lib.load()
 lib.la2_set_trace.argtypes = [ctypes.c_void_p]
-B, H = 8, 16
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+H = int(sys.argv[4]) if len(sys.argv) > 4 else 16
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 D = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 dev = torch.device('cuda', 0)
