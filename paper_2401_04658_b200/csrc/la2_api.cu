@@ -101,12 +101,11 @@ static int bind_device(void* stream, const void* ptr) {
   if (e != cudaSuccess) return set_cuda_error("cudaPointerGetAttributes", e);
   if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
     return set_error(LA2_ERR_VALUE, "tensor pointer is not device memory");
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != at.device) {
-    e = cudaSetDevice(at.device);
-    if (e != cudaSuccess) return set_cuda_error("cudaSetDevice", e);
-  }
+  // Always (re)bind: besides selecting the device this makes the primary context
+  // current on the calling thread, which the driver-API tensor-map encoder needs (the
+  // autograd engine runs the backward on its own thread).
+  e = cudaSetDevice(at.device);
+  if (e != cudaSuccess) return set_cuda_error("cudaSetDevice", e);
   return 0;
 }
 

@@ -793,11 +793,14 @@ template <int DK, bool REV, bool SO, int CM>
 static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullptr) {
   using L = TcLayout<DK, SO>;
   auto kern = la2_tc_kernel<DK, REV, SO, CM>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-  if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tc)", e);
-  if (CM != 0) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    (void)e;
+  cudaError_t e = cudaSuccess;
+  static int attr_dev = -1;  // attributes are per device; set once (they cost a driver call)
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (attr_dev != cur_dev) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tc)", e);
+    attr_dev = cur_dev;
   }
   // maps: q k v o of the pass, and of the sibling pass (CM 2: q1/o1 only; CM 3: all four)
   CUtensorMap mq, mk, mv, mo, mq1, mk1, mv1, mo1;

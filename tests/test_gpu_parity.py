@@ -452,3 +452,22 @@ def test_fused_backward_quad_bitwise(B, H, N):
     rq, rk, rv = port.bhnd_backward(to64(q), to64(k), to64(v), to64(do), decay)
     errs = {"dq": rel(c[0], rq), "dk": rel(c[1], rk), "dv": rel(c[2], rv)}
     assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_autograd_backward_on_fresh_thread():
+    """Regression: in a fresh process the autograd engine runs the first backward on its
+    own thread; the C ABI must bind the device/context there itself (d = 64 and 128)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = (
+        "import torch, paper_2401_04658_b200 as la2\n"
+        "for d in (64, 128):\n"
+        "    q, k, v = (torch.rand(1, 2, 256, d, device='cuda').bfloat16().requires_grad_() for _ in range(3))\n"
+        "    la2.lightning_attn2(q, k, v, [0.9, 1.0]).sum().backward()\n"
+        "    torch.cuda.synchronize()\n"
+        "    assert torch.isfinite(q.grad.float()).all()\n"
+        "print('ok')\n")
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
