@@ -125,9 +125,10 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *   LA2_TUNE_PREFETCH    L2 prefetch distance in blocks for 2-stage rings (default 0).
  *   LA2_TUNE_L2HINT      L2 policy bits: 1 loads evict_first, 2 prefetches evict_last,
  *                        4 output stores evict_first (default 0).
- *   LA2_TUNE_FUSED_BWD   1 (default): at d = dv = 128 the dV and dK scans of the backward
- *                        run as one 4-CTA cluster per unit sharing Q / dO through L2;
- *                        0: two separate launches.
+ *   LA2_TUNE_FUSED_BWD   1 (default): at d = dv = 128 with few heads (each pass alone
+ *                        would leave SMs idle) the dV and dK scans of the backward run as
+ *                        one 4-CTA cluster per unit sharing Q / dO through L2;
+ *                        0: always two separate launches.
  */
 #define LA2_TUNE_PERSISTENT 1
 #define LA2_TUNE_PREFETCH 2

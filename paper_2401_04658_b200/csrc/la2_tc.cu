@@ -937,7 +937,15 @@ int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
 // passes read are fetched from HBM once and hit L2 for the second pass.
 int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
   if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
-  if (!clusters_enabled() || !quad_enabled()) {
+  // The quad only pays when each pass alone leaves SMs idle (few heads, e.g. a long
+  // single sequence): with >= 148 / 4 pair units per pass two separate persistent
+  // launches keep every SM busy and the kernels are not DRAM-bound enough for the
+  // saved Q/dO reads to matter (ncu: 1117 us quad vs 2 x 520 us at B=8 H=16 N=16K).
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pair_units = adv.B * adv.H * (adv.dv / DVS) / 2;
+  if (!clusters_enabled() || !quad_enabled() || pair_units * 4 > sms) {
     if (int rc = launch_tc(adk, st)) return rc;
     return launch_tc(adv, st);
   }

@@ -430,7 +430,7 @@ def test_persistent_schedule_bitwise(B, H, N, d, dv):
     assert max(rel(a[0], ro), rel(a[1], rkv)) <= BF16_TOL
 
 
-@pytest.mark.parametrize("B,H,N", [(1, 3, 700), (2, 40, 300)])
+@pytest.mark.parametrize("B,H,N", [(1, 3, 700), (1, 35, 300)])  # 35 units > co-resident quads
 def test_fused_backward_quad_bitwise(B, H, N):
     """d = dv = 128: the dV/dK scans as one 4-CTA cluster (shared Q / dO through L2) give
     bitwise the same gradients as two separate launches, and match the oracle."""

@@ -16,8 +16,9 @@ KEYS = {
     "smem_bytes": ("launch__shared_mem_per_block_dynamic", 1),
 }
 def unit_scale(u):
-    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e3, "msecond": 1e6,
-            "nsecond": 1, "%": 1, "": 1}.get(u, 1)
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3,
+            "us": 1e3, "ms": 1e6, "ns": 1, "usecond": 1e3, "msecond": 1e6, "nsecond": 1,
+            "%": 1, "": 1}.get(u, 1)
 def load(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
