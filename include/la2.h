@@ -129,11 +129,15 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *                        would leave SMs idle) the dV and dK scans of the backward run as
  *                        one 4-CTA cluster per unit sharing Q / dO through L2;
  *                        0: always two separate launches.
+ *   LA2_TUNE_CONCURRENT_BWD  sequences with N <= value (default 8192) run the dQ scan of
+ *                        la2_backward on a forked side stream, concurrent with the dK/dV
+ *                        scans (joined back before return); 0 disables.
  */
 #define LA2_TUNE_PERSISTENT 1
 #define LA2_TUNE_PREFETCH 2
 #define LA2_TUNE_L2HINT 3
 #define LA2_TUNE_FUSED_BWD 4
+#define LA2_TUNE_CONCURRENT_BWD 5
 LA2_API int la2_set_tuning(int key, int value);
 
 /*

@@ -63,6 +63,45 @@ Workspace get_workspace(cudaStream_t st) {
   return w;
 }
 
+// Per-device side stream (non-blocking) + fork/join events for the concurrent dQ pass.
+// Fork/join through events is also valid inside CUDA graph capture.
+struct SideStream {
+  cudaStream_t s;
+  cudaEvent_t fork, join;
+};
+static SideStream* side_stream(cudaStream_t caller) {
+  static std::mutex mu;
+  static SideStream per_dev[16];
+  static bool made[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!made[dev]) {
+    // never create inside a graph capture (it would invalidate the capture): the first
+    // captured backward simply runs serially
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(caller, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    SideStream& x = per_dev[dev];
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    made[dev] = true;
+  }
+  return &per_dev[dev];
+}
+static int join_side(SideStream* side, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(side->join, side->s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, side->join, 0);
+  if (e != cudaSuccess) return set_cuda_error("side-stream join", e);
+  return 0;
+}
+
 static bool tc_eligible(int dtype, int dk, int dv) {
   return dtype == LA2_BF16 && (dk == 64 || dk == 128) && dv % 64 == 0 && dv >= 64 && dv <= 256;
 }
@@ -135,6 +174,11 @@ int la2_forward(const void* q, const void* k, const void* v, const float* decay,
   return run_f(a, static_cast<cudaStream_t>(stream));
 }
 
+static int backward_reverse(const void* q, const void* k, const void* v, const void* dout,
+                            const float* decay, void* dk, void* dv, const float* dkv_in,
+                            float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,
+                            cudaStream_t st);
+
 int la2_backward(const void* q, const void* k, const void* v, const void* dout, const float* decay,
                  void* dq, void* dk, void* dv, const float* kv_in, const float* dkv_in,
                  float* dkv_out, int B, int H, int N, int d, int dvd, int dtype, void* stream) {
@@ -146,8 +190,33 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
   if (int rc = bind_device(stream, q)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // dQ = F(dO, V, K): forward scan, state KV^T  (tiled_backward sweep 1, kernel.py:184-204)
+  // It shares no output with the dK/dV scans, so for short sequences (where each launch
+  // is dominated by its fill / drain) it runs on a forked side stream concurrently.
   FArgs aq{dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, dtype, 0};
-  if (int rc = run_f(aq, st)) return rc;
+  SideStream* side = (tuning_value(LA2_TUNE_CONCURRENT_BWD) > 0 &&
+                      N <= tuning_value(LA2_TUNE_CONCURRENT_BWD)) ? side_stream(st) : nullptr;
+  if (side != nullptr) {
+    if (cudaEventRecord(side->fork, st) != cudaSuccess || cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess) {
+      cudaGetLastError();
+      side = nullptr;
+    }
+  }
+  if (int rc = run_f(aq, side ? side->s : st)) {
+    if (side) join_side(side, st);
+    return rc;
+  }
+  const int rc = backward_reverse(q, k, v, dout, decay, dk, dv, dkv_in, dkv_out, B, H, N, d, dvd, dtype, st);
+  if (side) {
+    if (int jr = join_side(side, st)) return rc ? rc : jr;
+  }
+  return rc;
+}
+
+// dK and dV: the reverse sweep of tiled_backward (kernel.py:207-231).
+static int backward_reverse(const void* q, const void* k, const void* v, const void* dout,
+                            const float* decay, void* dk, void* dv, const float* dkv_in,
+                            float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,
+                            cudaStream_t st) {
   // d = dv = 64 bf16: dK and dV in one fused reverse scan (sweep 2, kernel.py:207-231)
   // (experimental single-kernel dK/dV scan, la2_bwd.cu; opt-in: slower than the pair below)
   static const bool fused_g = std::getenv("LA2_FUSED_BWD_G") != nullptr;

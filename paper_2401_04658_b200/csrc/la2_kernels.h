@@ -70,6 +70,7 @@ struct Workspace {
 Workspace get_workspace(cudaStream_t st);
 
 int set_tuning(int key, int value);
+int tuning_value(int key);
 int set_error(int code, const char* msg);
 int set_cuda_error(const char* where, cudaError_t e);
 

@@ -779,8 +779,20 @@ static bool persistent_enabled() { return g_persistent != 0; }
 static bool quad_enabled() { return g_quad != 0; }
 static int prefetch_blocks() { return g_prefetch; }
 static int l2_hints() { return g_l2hint; }
+static int g_concurrent_bwd = env_int("LA2_CONC_BWD", 8192);
+int tuning_value(int key) {
+  switch (key) {
+    case LA2_TUNE_PERSISTENT: return g_persistent;
+    case LA2_TUNE_PREFETCH: return g_prefetch;
+    case LA2_TUNE_L2HINT: return g_l2hint;
+    case LA2_TUNE_FUSED_BWD: return g_quad;
+    case LA2_TUNE_CONCURRENT_BWD: return g_concurrent_bwd;
+    default: return 0;
+  }
+}
 int set_tuning(int key, int value) {
   switch (key) {
+    case LA2_TUNE_CONCURRENT_BWD: g_concurrent_bwd = value; return 0;
     case LA2_TUNE_PERSISTENT: g_persistent = value; return 0;
     case LA2_TUNE_PREFETCH: g_prefetch = value; return 0;
     case LA2_TUNE_L2HINT: g_l2hint = value; return 0;

@@ -471,3 +471,37 @@ def test_autograd_backward_on_fresh_thread():
     root = Path(__file__).resolve().parents[1]
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_concurrent_backward_and_graph_capture():
+    """The dQ scan on a forked side stream gives bitwise the same gradients as the serial
+    order, and the fork/join is capturable in a CUDA graph (replay == eager)."""
+    B, H, N, D = 2, 4, 640, 64
+    q, k, v, do = gpu(*inputs(B, H, N, D, D, torch.bfloat16, seed=77))
+    decay = la2.decay_tensor([0.9, 0.99, 0.999, 1.0], H, torch.device(DEV))
+    try:
+        la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 0)
+        a = la2.la2_backward(q, k, v, do, decay)
+        la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 1 << 30)
+        b = la2.la2_backward(q, k, v, do, decay)
+        torch.cuda.synchronize()
+        for n, x, y in zip(("dq", "dk", "dv"), a, b):
+            assert torch.equal(x, y), n
+        out = {}
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            la2.la2_backward(q, k, v, do, decay)  # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out["o"], _ = la2.la2_forward(q, k, v, decay)
+            out["dq"], out["dk"], out["dv"], _ = la2.la2_backward(q, k, v, do, decay)
+        g.replay()
+        torch.cuda.synchronize()
+        o_ref, _ = la2.la2_forward(q, k, v, decay)
+        assert torch.equal(out["o"], o_ref)
+        for n, y in zip(("dq", "dk", "dv"), b):
+            assert torch.equal(out[n], y), n
+    finally:
+        la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 8192)
