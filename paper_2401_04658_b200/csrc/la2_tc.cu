@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int CS = (CM == 3) ? 4 : (CL ? 2 : 1);  // CTAs per cluster
   static_assert(CM != 2 || (DK == 64 && REV && !SO), "backward pair needs d = dv = 64");
   static_assert(CM != 3 || (DK == 128 && REV && !SO), "backward quad needs d = dv = 128");
-  static_assert(!(CL && SO), "state-only passes run without clusters");
+  static_assert(!(SO && CM >= 2), "state-only passes run alone or as value-slice pairs");
   constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tma_prefetch_l2_3d(&tm_v, slice * DVS, b2 * BT, bh);
         } else if (CM == 1 || CM == 3) {
 #pragma unroll
-          for (int c = 0; c < DK / 64; ++c) tma_prefetch_l2_3d(prank ? mk : mq, c * 64, b2 * BT, bh);
+          for (int c = 0; c < DK / 64; ++c)
+            if (!SO || prank) tma_prefetch_l2_3d(prank ? mk : mq, c * 64, b2 * BT, bh);
           tma_prefetch_l2_3d(mv, slice * DVS, b2 * BT, bh);
         } else {
           tma_prefetch_l2_3d(mq, 0, b2 * BT, bh);
@@ -267,8 +268,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         } else if (CM == 1 || CM == 3) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
-            if (prank == 0) tma_load_3d_mc(dq + c * REGION, mq, fb, c * 64, row, bh, mcmask);
-            else tma_load_3d_mc(dk + c * REGION, mk, fb, c * 64, row, bh, mcmask);
+            if (prank == 0) {
+              if (!SO) tma_load_3d_mc(dq + c * REGION, mq, fb, c * 64, row, bh, mcmask);
+            } else {
+              tma_load_3d_mc(dk + c * REGION, mk, fb, c * 64, row, bh, mcmask);
+            }
           }
           tma_load_3d(dv, mv, fb, slice * DVS, row, bh);
         } else {
@@ -917,9 +921,11 @@ int launch_tc(const FArgs& a, cudaStream_t st) {
   if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
   const bool so = (a.o == nullptr);
   // value-slice pairs share their Q/K tiles through a 2-CTA cluster
-  const bool pair = !so && clusters_enabled() && (a.dv / DVS) % 2 == 0;
+  const bool pair = clusters_enabled() && (a.dv / DVS) % 2 == 0;
 #define LA2_TC_DISPATCH(DKV)                                                                   \
   if (a.dk == DKV) {                                                                           \
+    if (so && pair) return a.reverse ? launch_tc_t<DKV, true, true, 1>(a, st)                  \
+                                     : launch_tc_t<DKV, false, true, 1>(a, st);                \
     if (so) return a.reverse ? launch_tc_t<DKV, true, true, 0>(a, st)                          \
                              : launch_tc_t<DKV, false, true, 0>(a, st);                        \
     if (pair) return a.reverse ? launch_tc_t<DKV, true, false, 1>(a, st)                       \
