@@ -1,0 +1,253 @@
+"""GPU timing harness with the reference's record schema and scaling verdict.
+
+Mirrors ``tila.bench`` (pkg/src/tila/bench.py) for the B200 path so that the
+"flat in sequence length" claim is judged by the same automated rule the
+reference applies to its own CPU kernel:
+
+* ``CSV_HEADER`` / ``emit_csv``        -- bench.py:33, :301-314 (same columns/format)
+* ``classify`` and its bands          -- bench.py:35-36, :99-108
+* ``time_pass``                        -- bench.py:165-192 (median of >= 3 reps after a
+                                          warm-up; device time from CUDA events; the
+                                          scratch column is the device memory the pass
+                                          allocates beyond its inputs)
+* ``scaling_sweep`` / ``_check_n_list`` -- bench.py:230-261 (strictly doubling n, >= 4
+                                          points; "tiled" is timed fwd+bwd, "chunked" /
+                                          "recurrent" forward only, as SWEEP_DIRECTIONS)
+* ``block_size_sweep``                 -- bench.py:264-292 (results must not depend on
+                                          the block size; the GPU kernel picks its own
+                                          128-token tile, so every block gives the same
+                                          output and the rows time the same kernel)
+
+Implementations (``impl``): "tiled" = la2_forward / la2_backward on [1,1,n,d]
+tensors (the reference's single-head shape), "chunked" = STREAM_CHUNKS calls with
+the carried fp32 state, "recurrent" = one la2_decode_step per token. The
+reference's "oracle" (O(n^2) CPU) has no GPU counterpart here.
+
+Run: ``python -m paper_2401_04658_b200.gpubench --csv out.csv`` (prints the
+verdicts; exit code 0 when every implementation is linear-like, like
+``tila bench``'s acceptance check).
+"""
+
+from __future__ import annotations
+
+import argparse
+import math
+import statistics
+import sys
+from dataclasses import dataclass, field
+
+import torch
+
+from . import ops
+
+IMPLS = ("tiled", "chunked", "recurrent")
+DIRECTIONS = ("forward", "backward", "fwd+bwd")
+CSV_HEADER = "impl,direction,n,d,dv,B,lambda,reps,median_s,us_per_token,scratch_bytes"
+LINEAR_BAND = (1.5, 2.7)
+QUADRATIC_BAND = (3.2, 5.0)
+STREAM_CHUNKS = 4
+SWEEP_DIRECTIONS = {"recurrent": "forward", "tiled": "fwd+bwd", "chunked": "forward"}
+
+
+@dataclass
+class BenchRecord:
+    impl: str
+    direction: str
+    n: int
+    d: int
+    dv: int
+    block: int
+    lam: float
+    reps: int
+    median_seconds: float
+    per_token_microseconds: float
+    scratch_bytes: int
+    oom: bool = False
+
+
+@dataclass
+class ScalingVerdict:
+    impl: str
+    ratios: list = field(default_factory=list)
+    classification: str = "inconclusive"
+
+
+def classify(ratios) -> str:
+    """linear-like / quadratic-like / inconclusive from time-doubling ratios."""
+    ratios = list(ratios)
+    if not ratios or any(not math.isfinite(r) for r in ratios):
+        return "inconclusive"
+    if all(LINEAR_BAND[0] <= r <= LINEAR_BAND[1] for r in ratios):
+        return "linear-like"
+    if all(QUADRATIC_BAND[0] <= r <= QUADRATIC_BAND[1] for r in ratios):
+        return "quadratic-like"
+    return "inconclusive"
+
+
+def _check_n_list(n_list) -> list:
+    n_list = [int(n) for n in n_list]
+    if len(n_list) < 4:
+        raise ValueError("minimum 4 points required in the sequence-length sweep")
+    for a, b in zip(n_list, n_list[1:]):
+        if b != 2 * a:
+            raise ValueError(f"sequence lengths must strictly double, got {a} -> {b}")
+    return n_list
+
+
+def _inputs(n, d, dv, dtype, seed, device, heads=1, batch=1):
+    g = torch.Generator(device=device).manual_seed(int(seed) * 10)
+    mk = lambda c: (torch.rand(batch, heads, n, c, device=device, generator=g) * 2 - 1).to(dtype)
+    return mk(d), mk(d), mk(dv), mk(dv)
+
+
+def _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads=1, batch=1):
+    if impl not in IMPLS:
+        raise ValueError(f"unknown impl {impl!r}, expected one of {IMPLS}")
+    if direction not in DIRECTIONS:
+        raise ValueError(f"unknown direction {direction!r}, expected one of {DIRECTIONS}")
+    if impl in ("recurrent", "chunked") and direction != "forward":
+        raise ValueError(f"{impl} supports only the forward direction")
+    q, k, v, do = _inputs(n, d, dv, dtype, seed, device, heads, batch)
+    dec = ops.decay_tensor(lam, heads, device)
+
+    def forward():
+        if impl == "tiled":
+            ops.la2_forward(q, k, v, dec)
+        elif impl == "chunked":
+            state = None
+            edges = [n * i // STREAM_CHUNKS for i in range(STREAM_CHUNKS + 1)]
+            for a, b in zip(edges, edges[1:]):
+                if b > a:
+                    _, state = ops.la2_forward(q[:, :, a:b], k[:, :, a:b], v[:, :, a:b], dec,
+                                               kv_in=state, output_final_state=True)
+        else:
+            st = torch.zeros(batch, heads, d, dv, device=device)
+            for t in range(n):
+                ops.decode_step(q[:, :, t], k[:, :, t], v[:, :, t], dec, st)
+
+    def backward():
+        ops.la2_backward(q, k, v, do, dec)
+
+    if direction == "forward":
+        return forward
+    if direction == "backward":
+        return backward
+
+    def both():
+        forward()
+        backward()
+
+    return both
+
+
+def time_pass(impl: str, direction: str, n: int, d: int = 64, dv: int = None, block: int = 64,
+              lam: float = 0.9, reps: int = 5, seed: int = 0, dtype=torch.bfloat16,
+              device=None, heads: int = 1, batch: int = 1) -> BenchRecord:
+    """Median device time over ``reps`` runs after one warm-up (bench.py:165-192)."""
+    if reps < 3:
+        raise ValueError(f"reps must be >= 3, got {reps}")
+    if block < 1:
+        raise ValueError(f"block must be >= 1, got {block}")
+    dv = d if dv is None else dv
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    try:
+        run = _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads, batch)
+        torch.cuda.synchronize(device)
+        base = torch.cuda.memory_allocated(device)
+        torch.cuda.reset_peak_memory_stats(device)
+        run()
+        torch.cuda.synchronize(device)
+        scratch = max(0, torch.cuda.max_memory_allocated(device) - base)
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    except torch.cuda.OutOfMemoryError:
+        return BenchRecord(impl, direction, n, d, dv, block, lam, reps, float("nan"),
+                           float("nan"), 0, oom=True)
+    median = statistics.median(times)
+    return BenchRecord(impl, direction, n, d, dv, block, lam, reps, median, median * 1e6 / n,
+                       int(scratch))
+
+
+def scaling_sweep(impls, n_list, d: int = 64, block: int = 64, lam: float = 0.9, reps: int = 5,
+                  seed: int = 0, dtype=torch.bfloat16, heads: int = 1, batch: int = 1):
+    """Time each implementation over a doubling n-sweep and classify it (bench.py:237-261)."""
+    n_list = _check_n_list(n_list)
+    records, verdicts = [], []
+    for impl in impls:
+        direction = SWEEP_DIRECTIONS.get(impl)
+        if direction is None:
+            raise ValueError(f"unknown impl {impl!r}, expected one of {IMPLS}")
+        rows = [time_pass(impl, direction, n, d, d, block, lam, reps, seed, dtype,
+                          heads=heads, batch=batch) for n in n_list]
+        records.extend(rows)
+        times = [r.median_seconds for r in rows]
+        ratios = [b / a if a > 0 else float("nan") for a, b in zip(times, times[1:])]
+        verdicts.append(ScalingVerdict(impl, ratios, classify(ratios)))
+    return records, verdicts
+
+
+def block_size_sweep(n: int, d: int, lam: float, blocks, reps: int = 5, seed: int = 0,
+                     dtype=torch.bfloat16):
+    """bench.py:264-292: outputs must be block-size invariant; then time each block."""
+    blocks = [int(b) for b in blocks]
+    if not blocks:
+        raise ValueError("at least one block size required")
+    for b in blocks:
+        if b < 1:
+            raise ValueError(f"block must be >= 1, got {b}")
+    device = torch.device("cuda", torch.cuda.current_device())
+    q, k, v, _ = _inputs(n, d, d, dtype, seed, device)
+    dec = ops.decay_tensor(lam, 1, device)
+    ref, _ = ops.la2_forward(q, k, v, dec)
+    for b in blocks[1:]:
+        out, _ = ops.la2_forward(q, k, v, dec)
+        if not torch.equal(out, ref):
+            raise ValueError(f"block size {b} changed the output vs block size {blocks[0]}")
+    return [time_pass("tiled", "forward", n, d, d, b, lam, reps, seed, dtype) for b in blocks]
+
+
+def _fmt(x) -> str:
+    return format(x, ".17g") if isinstance(x, float) else str(x)
+
+
+def emit_csv(records, path) -> None:
+    """Same header and decimal formatting as bench.py:301-314."""
+    records = list(records)
+    if not records:
+        raise ValueError("nothing to emit")
+    with open(path, "w", encoding="ascii", newline="") as fh:
+        fh.write(CSV_HEADER + "\n")
+        for r in records:
+            fh.write(",".join([r.impl, r.direction, str(r.n), str(r.d), str(r.dv), str(r.block),
+                               _fmt(r.lam), str(r.reps), _fmt(r.median_seconds),
+                               _fmt(r.per_token_microseconds), str(r.scratch_bytes)]) + "\n")
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description="GPU scaling sweep with the reference verdict")
+    ap.add_argument("--impls", default="tiled,chunked")
+    ap.add_argument("--n", default="1024,2048,4096,8192,16384,32768,65536")
+    ap.add_argument("--d", type=int, default=64)
+    ap.add_argument("--heads", type=int, default=128,
+                    help="heads per call (the reference times one head; one B200 needs ~128)")
+    ap.add_argument("--lam", type=float, default=0.9)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--csv", default=None)
+    a = ap.parse_args(argv)
+    records, verdicts = scaling_sweep(a.impls.split(","), [int(x) for x in a.n.split(",")], a.d,
+                                      lam=a.lam, reps=a.reps, heads=a.heads)
+    if a.csv:
+        emit_csv(records, a.csv)
+    for v in verdicts:
+        print(f"{v.impl}: {v.classification} (doubling ratios {', '.join(f'{r:.2f}' for r in v.ratios)})")
+    return 0 if all(v.classification == "linear-like" for v in verdicts) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -107,15 +107,21 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     One CTA owns one (b, h, 64-wide value slice) for the whole sequence, so with
     fewer units than SMs the GPU idles. Viewing [B,H,N,d] as [B,H*G,N/G,d] (a free
     reshape) gives G x more units at the cost of one state-only pass over K,V (and
-    Q,dO in the backward). Used when units < ~100 and chunks stay >= 2048 tokens.
+    Q,dO in the backward). Tensor-core path: used when units < ~100 and chunks stay
+    >= 2048 tokens. SIMT path (fp32 / other shapes, several CTAs per SM): split until
+    ~4 units per SM with chunks >= 256 tokens.
     """
-    if dtype != torch.bfloat16 or d not in (64, 128) or dv % 64:
-        return 1
-    units = B * H * (dv // 64)
-    if units >= 100:
-        return 1
+    units = B * H * ((dv + 63) // 64)
     g = 1
-    while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 2048:
+    if dtype == torch.bfloat16 and d in (64, 128) and dv % 64 == 0:
+        if units >= 100:
+            return 1
+        while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 2048:
+            g *= 2
+        return g
+    if d > 256 or dv > 256:
+        return 1
+    while units * g < 4 * NUM_SMS and N % (2 * g) == 0 and N // (2 * g) >= 256:
         g *= 2
     return g
 

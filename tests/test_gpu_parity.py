@@ -505,3 +505,31 @@ def test_concurrent_backward_and_graph_capture():
             assert torch.equal(out[n], y), n
     finally:
         la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 8192)
+
+
+def test_fp32_autograd_auto_split_c1():
+    """C1 in fp32 through the autograd entry point: the SIMT path splits the sequence
+    (split_factor = 8) and still meets the 1e-4 gate for o, dq, dk, dv."""
+    B, H, N, D = 1, 8, 2048, 64
+    assert la2.split_factor(B, H, N, D, D, torch.float32) == 8
+    q, k, v, do = inputs(B, H, N, D, D, torch.float32, seed=12)
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    o = la2.lightning_attn2(qg, kg, vg, C1_DECAY)
+    o.backward(do.to(DEV))
+    ro = port.bhnd_oracle_forward(to64(q), to64(k), to64(v), C1_DECAY)
+    rq, rk, rv = port.bhnd_oracle_backward(to64(q), to64(k), to64(v), to64(do), C1_DECAY)
+    errs = {"o": rel(o, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
+    assert max(errs.values()) <= FP32_TOL, errs
+
+
+def test_gpubench_sweep_and_block_invariance():
+    """GPU harness: a doubling sweep yields one record per (impl, n) and a verdict;
+    block sizes never change results (bench.py:264-292)."""
+    from paper_2401_04658_b200 import gpubench as gb
+    recs, verdicts = gb.scaling_sweep(["tiled", "chunked"], [256, 512, 1024, 2048], 64,
+                                      reps=3, heads=4)
+    assert len(recs) == 8 and [v.impl for v in verdicts] == ["tiled", "chunked"]
+    assert all(r.median_seconds > 0 and not r.oom for r in recs)
+    assert all(len(v.ratios) == 3 for v in verdicts)
+    rows = gb.block_size_sweep(512, 64, 0.9, [16, 64, 256], reps=3)
+    assert [r.block for r in rows] == [16, 64, 256]

@@ -65,3 +65,40 @@ def test_tila_api_validation_matches_reference():
 def test_tila_api_requires_gpu():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         tila_api.tiled_forward(np.ones((2, 3)), np.ones((2, 3)), np.ones((2, 3)), 0.5, 4)
+
+
+def test_split_factor_policy():
+    """Intra-GPU sequence split: tensor-core shapes split only when units underfill the
+    GPU (chunks >= 2048 tokens); SIMT shapes (fp32) split to ~4 units per SM (>= 256)."""
+    import torch
+    from paper_2401_04658_b200.ops import split_factor
+    assert split_factor(8, 16, 65536, 64, 64, torch.bfloat16) == 1        # C2: 128 units
+    assert split_factor(1, 16, 524288, 128, 128, torch.bfloat16) == 8     # C5 on one GPU
+    assert split_factor(1, 2, 300, 64, 64, torch.bfloat16) == 1           # too short
+    assert split_factor(1, 8, 2048, 64, 64, torch.float32) == 8           # C1 fp32 (SIMT)
+    assert split_factor(1, 3, 333, 4, 7, torch.float32) == 1              # odd length
+    assert split_factor(64, 16, 4096, 64, 64, torch.float32) == 1         # already 1024 units
+
+
+def test_gpubench_verdict_and_csv(tmp_path):
+    """The GPU harness keeps the reference's classify bands, sweep rule and CSV schema
+    (pkg/src/tila/bench.py:33-36, :99-108, :230-235, :301-314)."""
+    from paper_2401_04658_b200 import gpubench as gb
+    assert gb.CSV_HEADER == "impl,direction,n,d,dv,B,lambda,reps,median_s,us_per_token,scratch_bytes"
+    assert gb.classify([2.0, 2.1, 1.9]) == "linear-like"
+    assert gb.classify([4.0, 4.1]) == "quadratic-like"
+    assert gb.classify([2.0, 4.0]) == "inconclusive"
+    assert gb.classify([]) == "inconclusive"
+    assert gb.classify([float("nan")]) == "inconclusive"
+    with pytest.raises(ValueError):
+        gb._check_n_list([128, 256, 512])
+    with pytest.raises(ValueError):
+        gb._check_n_list([128, 256, 500, 1000])
+    rec = gb.BenchRecord("tiled", "fwd+bwd", 1024, 64, 64, 64, 0.9, 5, 1e-4, 0.1, 0)
+    p = tmp_path / "x.csv"
+    gb.emit_csv([rec], p)
+    lines = p.read_text().splitlines()
+    assert lines[0] == gb.CSV_HEADER
+    assert lines[1] == "tiled,fwd+bwd,1024,64,64,64,0.90000000000000002,5,0.0001,0.10000000000000001,0"
+    with pytest.raises(ValueError):
+        gb.emit_csv([], p)
