@@ -52,8 +52,9 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tbase = *slot;
   const bool a_tmem = (a_mn == 2);
   if (a_tmem) {
-    // A row m -> TMEM lane m, columns 128.. as packed bf16 pairs (K-major)
-    const int m = (warp & 3) * 32 + lane;
+    // A row m -> TMEM lane m (M = 128) or lane 32*(m/16) + m%16 (M = 64, the D layout
+    // of an M = 64 MMA), columns 128.. as packed bf16 pairs (K-major)
+    const int m = (M == 128) ? (warp & 3) * 32 + lane : (warp & 3) * 16 + (lane & 15);
     for (int c0 = 0; c0 < K / 2; c0 += 16) {
       uint32_t r[16];
       for (int j = 0; j < 16; ++j)
@@ -107,7 +108,6 @@ extern "C" LA2_API int la2_selftest_umma(const float* A, const float* B, float* 
   using namespace la2;
   if (!((M == 64 || M == 128) && (N == 64 || N == 128) && (K == 64 || K == 128)))
     return set_error(LA2_ERR_VALUE, "selftest: M,N in {64,128}, K in {64,128}");
-  if (a_mn == 2 && M != 128) return set_error(LA2_ERR_VALUE, "selftest: TMEM A needs M=128");
   const int smem = 65536 + 128 + 1024;
   cudaError_t e = cudaFuncSetAttribute(la2_umma_selftest_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -12,8 +12,9 @@ pytestmark = pytest.mark.gpu
 
 
 CASES = list(itertools.product((64, 128), (64, 128), (64, 128), (0, 1), (0, 1)))
-# a_mn == 2: A operand read from TMEM (tcgen05.mma ... [a_tmem]), M = 128 only
-CASES += list(itertools.product((128,), (64, 128), (64, 128), (2,), (0, 1)))
+# a_mn == 2: A operand read from TMEM (tcgen05.mma ... [a_tmem]); for M = 64 the A rows
+# sit in lanes 0-15 of each 32-lane quarter, like the M = 64 accumulator layout
+CASES += list(itertools.product((64, 128), (64, 128), (64, 128), (2,), (0, 1)))
 
 
 @pytest.mark.parametrize("M,N,K,a_mn,b_mn", CASES)
