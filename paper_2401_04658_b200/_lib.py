@@ -74,5 +74,13 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what}: {msg} (code {rc})")
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
+    if rc:
+        check(rc, name)

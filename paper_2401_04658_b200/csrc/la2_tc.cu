@@ -753,8 +753,29 @@ static int get_encode() {
 // [BH][N][cols] bf16, box (64 cols, 128 rows, 1 head), 128B swizzle.
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows);
 int tma_encoder_ready() { return get_encode(); }
+// Tensor maps depend only on (address, shape, box), so they are cached per host thread
+// (a map for the same address and shape is valid whatever tensor now lives there).
 static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT) {
-  return make_tmap_bf16(m, ptr, cols, N, BH, box_rows);
+  struct Entry {
+    const void* ptr;
+    int cols, N, BH, box;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[32];
+  static thread_local int next = 0;
+  for (const Entry& e : cache) {
+    if (e.ptr == ptr && e.cols == cols && e.N == N && e.BH == BH && e.box == box_rows && ptr) {
+      *m = e.map;
+      return 0;
+    }
+  }
+  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows);
+  if (rc == 0) {
+    Entry& e = cache[next];
+    next = (next + 1) & 31;
+    e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.map = *m;
+  }
+  return rc;
 }
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
