@@ -698,13 +698,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (warp == W0) TR(3, i, 4);
         tc_fence_after();
 #pragma unroll
-        for (int q = 0; q < DVS / 16; ++q) {
-          float d16[16];
-          tmem_ld16(tbase + L::T_KV + db * 64 + lane_off + q * 16, d16);
+        for (int q = 0; q < DVS / 32; ++q) {  // two 32-column loads: half the round trips
+          uint32_t d32[32];
+          tmem_ld32_raw(tbase + L::T_KV + db * 64 + lane_off + q * 32, d32);
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) kv[16 * q + e] = fmaf(fr, kv[16 * q + e], d16[e]);
+            for (int e = 0; e < 32; ++e) kv[32 * q + e] = fmaf(fr, kv[32 * q + e], __uint_as_float(d32[e]));
           }
         }
         tc_fence_before();
