@@ -63,6 +63,10 @@ def exclusive_scan(state: torch.Tensor, decay: torch.Tensor, length: int, group=
     G = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = state.device
+    if state.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host memory only: stage the (small, [B,H,d,dv]) state through the host
+        out = exclusive_scan(state.cpu(), decay.cpu(), length, group, reverse, mode)
+        return out.to(dev)
     decay = decay.to(dev)
     lens = torch.tensor([length], dtype=torch.int64, device=dev)
     if G == 1:

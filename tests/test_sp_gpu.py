@@ -36,7 +36,9 @@ def _worker(rank, world, port_no, mode, d, result_q):
         o = la2.sp_lightning_attn2(qg, kg, vg, decay.to(dev), mode=mode)
         o.backward(do[:, :, sl].to(dev))
         torch.cuda.synchronize()
-        result_q.put((rank, o.detach().cpu(), qg.grad.cpu(), kg.grad.cpu(), vg.grad.cpu()))
+        # numpy copies: torch tensors would travel as shared-memory handles that die with
+        # this process
+        result_q.put((rank, *(t.detach().float().cpu().numpy() for t in (o, qg.grad, kg.grad, vg.grad))))
     except Exception as e:  # pragma: no cover - surfaced by the parent
         result_q.put((rank, repr(e), None, None, None))
     finally:
@@ -64,7 +66,7 @@ def test_sp_two_ranks_match_unsharded(mode, d):
             if "gloo" in res[r][0].lower() and "cuda" in res[r][0].lower():
                 pytest.skip(f"gloo cannot exchange CUDA tensors here: {res[r][0]}")
             raise AssertionError(res[r][0])
-    o, dq, dk, dv = (torch.cat([res[r][i] for r in range(world)], dim=2) for i in range(4))
+    o, dq, dk, dv = (torch.cat([torch.from_numpy(res[r][i]) for r in range(world)], dim=2) for i in range(4))
     torch.manual_seed(0)
     B, H, N = 1, 4, 1024 * world
     dev = torch.device("cuda", 0)
