@@ -27,6 +27,12 @@
 //   warps 2-9  row warps:   thread <-> token row, two warps per TMEM lane quarter
 //              splitting the columns; S -> P, O epilogue + TMA store
 //   warps 10-13 state warps: V~ rows, dKV -> fp32 KV state -> bf16 KV operand
+//
+// Scheduling: a persistent stream-K split of the (recurrence, block) space over the
+// co-resident CTAs/clusters (Sched, la2_tc_common.cuh) when there are more recurrences
+// than SMs; the producer walks the range and publishes a per-block record (head, block,
+// segment start/end) in smem so the other roles carry no schedule state.
+// d = 128: O lives in the upper half of its S buffer (OIS), so O is double-buffered.
 #include <cudaTypedefs.h>
 
 #include <cstdio>
