@@ -132,12 +132,17 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *   LA2_TUNE_CONCURRENT_BWD  sequences with N <= value (default 8192) run the dQ scan of
  *                        la2_backward on a forked side stream, concurrent with the dK/dV
  *                        scans (joined back before return); 0 disables.
+ *   LA2_TUNE_PARTITION_BWD   d = 64 sequences with N <= value (default 32768) run the dQ
+ *                        scan and the dK/dV pair concurrently on disjoint SM partitions
+ *                        (1/3 : 2/3, both persistent); 0 disables (then the
+ *                        LA2_TUNE_CONCURRENT_BWD rule applies).
  */
 #define LA2_TUNE_PERSISTENT 1
 #define LA2_TUNE_PREFETCH 2
 #define LA2_TUNE_L2HINT 3
 #define LA2_TUNE_FUSED_BWD 4
 #define LA2_TUNE_CONCURRENT_BWD 5
+#define LA2_TUNE_PARTITION_BWD 6
 LA2_API int la2_set_tuning(int key, int value);
 
 /*

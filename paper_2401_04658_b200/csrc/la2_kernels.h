@@ -22,6 +22,7 @@ struct FArgs {
   int B, H, N, dk, dv;
   int dtype;
   int reverse;
+  int max_ranges = 0;  // persistent schedule: cap on co-resident work ranges (0 = all SMs)
 };
 
 // Kernel-side parameter block (passed by value).

@@ -811,6 +811,7 @@ static bool quad_enabled() { return g_quad != 0; }
 static int prefetch_blocks() { return g_prefetch; }
 static int l2_hints() { return g_l2hint; }
 static int g_concurrent_bwd = env_int("LA2_CONC_BWD", 8192);
+static int g_partition_bwd = env_int("LA2_PARTITION_BWD", 32768);
 int tuning_value(int key) {
   switch (key) {
     case LA2_TUNE_PERSISTENT: return g_persistent;
@@ -818,12 +819,14 @@ int tuning_value(int key) {
     case LA2_TUNE_L2HINT: return g_l2hint;
     case LA2_TUNE_FUSED_BWD: return g_quad;
     case LA2_TUNE_CONCURRENT_BWD: return g_concurrent_bwd;
+    case LA2_TUNE_PARTITION_BWD: return g_partition_bwd;
     default: return 0;
   }
 }
 int set_tuning(int key, int value) {
   switch (key) {
     case LA2_TUNE_CONCURRENT_BWD: g_concurrent_bwd = value; return 0;
+    case LA2_TUNE_PARTITION_BWD: g_partition_bwd = value; return 0;
     case LA2_TUNE_PERSISTENT: g_persistent = value; return 0;
     case LA2_TUNE_PREFETCH: g_prefetch = value; return 0;
     case LA2_TUNE_L2HINT: g_l2hint = value; return 0;
@@ -913,10 +916,11 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
       cudaGetLastError();
       max_ranges = n;
     }
-    if (max_ranges > 0 && p.units > max_ranges) {
+    const int cap = (a.max_ranges > 0 && a.max_ranges < max_ranges) ? a.max_ranges : max_ranges;
+    if (cap > 0 && p.units > cap) {
       const Workspace w = get_workspace(st);
-      if (w.ws != nullptr && w.slots >= max_ranges * CS) {
-        p.P = max_ranges;
+      if (w.ws != nullptr && w.slots >= cap * CS) {
+        p.P = cap;
         p.ws = w.ws;
         p.flags = w.flags;
       }

@@ -533,3 +533,21 @@ def test_gpubench_sweep_and_block_invariance():
     assert all(len(v.ratios) == 3 for v in verdicts)
     rows = gb.block_size_sweep(512, 64, 0.9, [16, 64, 256], reps=3)
     assert [r.block for r in rows] == [16, 64, 256]
+
+
+def test_partitioned_backward_bitwise():
+    """d = 64: the dQ scan and the dK/dV pair run concurrently on disjoint SM partitions
+    (both persistent, capped ranges) -- gradients bitwise equal to the serial order."""
+    B, H, N, D = 1, 64, 8320, 64
+    q, k, v, do = gpu(*inputs(B, H, N, D, D, torch.bfloat16, seed=5))
+    decay = la2.decay_tensor(list(np.linspace(0.9, 1.0, H)), H, torch.device(DEV))
+    try:
+        la2.set_tuning(la2.ops.TUNE_PARTITION_BWD, 1 << 30)
+        a = la2.la2_backward(q, k, v, do, decay)
+        la2.set_tuning(la2.ops.TUNE_PARTITION_BWD, 0)
+        b = la2.la2_backward(q, k, v, do, decay)
+        torch.cuda.synchronize()
+    finally:
+        la2.set_tuning(la2.ops.TUNE_PARTITION_BWD, 32768)
+    for n, x, y in zip(("dq", "dk", "dv"), a, b):
+        assert torch.equal(x, y), n
