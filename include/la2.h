@@ -129,10 +129,10 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *                        would leave SMs idle) the dV and dK scans of the backward run as
  *                        one 4-CTA cluster per unit sharing Q / dO through L2;
  *                        0: always two separate launches.
- *   LA2_TUNE_CONCURRENT_BWD  sequences with N <= value (default 8192) run the dQ scan of
+ *   LA2_TUNE_CONCURRENT_BWD  sequences with N <= value (default 16384) run the dQ scan of
  *                        la2_backward on a forked side stream, concurrent with the dK/dV
  *                        scans (joined back before return); 0 disables.
- *   LA2_TUNE_PARTITION_BWD   d = 64 sequences with N <= value (default 32768) run the dQ
+ *   LA2_TUNE_PARTITION_BWD   d = 64 sequences with N <= value (default 8192) run the dQ
  *                        scan and the dK/dV pair concurrently on disjoint SM partitions
  *                        (1/3 : 2/3, both persistent); 0 disables (then the
  *                        LA2_TUNE_CONCURRENT_BWD rule applies).

@@ -201,7 +201,7 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
   // (dQ = 1 scan, the pair = 2 scans): the pair gets 2/3 of the SMs as clusters and is
   // launched first, the dQ scan takes the rest; both keep the persistent schedule inside
   // their partition. Measured (B=8 H=16): -11 % at N=1K, -2.5 % at 16K, +3 % at 64K, so
-  // it is used up to N = LA2_TUNE_PARTITION_BWD (default 32768).
+  // it is used up to N = LA2_TUNE_PARTITION_BWD (default 8192).
   if (dtype == LA2_BF16 && d == 64 && dvd == 64 && N <= tuning_value(LA2_TUNE_PARTITION_BWD)) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

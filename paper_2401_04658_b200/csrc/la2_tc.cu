@@ -810,8 +810,8 @@ static bool persistent_enabled() { return g_persistent != 0; }
 static bool quad_enabled() { return g_quad != 0; }
 static int prefetch_blocks() { return g_prefetch; }
 static int l2_hints() { return g_l2hint; }
-static int g_concurrent_bwd = env_int("LA2_CONC_BWD", 8192);
-static int g_partition_bwd = env_int("LA2_PARTITION_BWD", 32768);
+static int g_concurrent_bwd = env_int("LA2_CONC_BWD", 16384);
+static int g_partition_bwd = env_int("LA2_PARTITION_BWD", 8192);
 int tuning_value(int key) {
   switch (key) {
     case LA2_TUNE_PERSISTENT: return g_persistent;

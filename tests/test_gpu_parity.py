@@ -504,7 +504,7 @@ def test_concurrent_backward_and_graph_capture():
         for n, y in zip(("dq", "dk", "dv"), b):
             assert torch.equal(out[n], y), n
     finally:
-        la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 8192)
+        la2.set_tuning(la2.ops.TUNE_CONCURRENT_BWD, 16384)
 
 
 def test_fp32_autograd_auto_split_c1():
@@ -548,6 +548,14 @@ def test_partitioned_backward_bitwise():
         b = la2.la2_backward(q, k, v, do, decay)
         torch.cuda.synchronize()
     finally:
-        la2.set_tuning(la2.ops.TUNE_PARTITION_BWD, 32768)
+        la2.set_tuning(la2.ops.TUNE_PARTITION_BWD, 8192)
     for n, x, y in zip(("dq", "dk", "dv"), a, b):
         assert torch.equal(x, y), n
+
+
+def test_cli_verify_gradcheck_stream_demo():
+    """The operator CLI (reference cli.py retargeted to the GPU) passes on the small grid."""
+    from paper_2401_04658_b200 import cli
+    assert cli.main(["verify", "--grid", "small", "--seed", "3"]) == 0
+    assert cli.main(["gradcheck"]) == 0
+    assert cli.main(["stream-demo", "--dim", "64", "--chunk", "300", "--chunks", "4"]) == 0

@@ -102,3 +102,17 @@ def test_gpubench_verdict_and_csv(tmp_path):
     assert lines[1] == "tiled,fwd+bwd,1024,64,64,64,0.90000000000000002,5,0.0001,0.10000000000000001,0"
     with pytest.raises(ValueError):
         gb.emit_csv([], p)
+
+
+def test_cli_usage_errors_exit_2():
+    """CLI parity with the reference (pkg/src/tila/cli.py): bad sweeps are usage errors."""
+    from paper_2401_04658_b200 import cli
+    for argv in (["bench", "--impls", "tiled", "--lens", "128,256,512", "--dim", "64", "--block", "64"],
+                 ["bench", "--impls", "tiled", "--lens", "128,256,500,1000", "--dim", "64", "--block", "64"],
+                 ["bench", "--impls", "oracle", "--lens", "128,256,512,1024", "--dim", "64", "--block", "64"],
+                 ["nope"]):
+        with pytest.raises(SystemExit) as e:
+            cli.main(argv)
+        assert e.value.code == 2
+    args = cli.build_parser().parse_args(["stream-demo", "--dim", "64", "--chunk", "100", "--chunks", "3"])
+    assert args.lam == cli.BENCH_LAMBDA
