@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(g::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_COUNT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TR_INIT;
   const int h = blockIdx.y;
   const int bh = blockIdx.z * p.H + h;
   const int N = p.N;

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  TR_INIT;
   const uint32_t crank = CL ? cluster_ctarank() : 0;
   // CM 3: ranks 0-1 run one pass (value-slice pair), ranks 2-3 the sibling pass
   const int pair = (CM == 3) ? static_cast<int>(crank >> 1) : 0;
@@ -342,9 +343,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int i = 0; i < T; ++i) {
           const int s = i % NS, b = i & 1;
           const uint64_t v = adv(dV0, s * L::V_BYTES);
+          TR(1, i, 0);
           if (i + 1 < T) issue_S(i + 1);
+          TR(1, i, 1);
           mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
+          TR(1, i, 2);
           if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          TR(1, i, 3);
           tc_fence_after();
           if (leader) {
 #pragma unroll

@@ -11,13 +11,20 @@ namespace la2 {
 #ifdef LA2_TRACE
 static __device__ long long* g_trace = nullptr;  // per translation unit
 constexpr int TR_MAXB = 64, TR_EV = 8;  // roles 0..4
+// TR_INIT caches the buffer pointer (and the "is CTA 0" test) in registers at kernel
+// start: re-reading the __device__ pointer per event put an L2 round trip on every stamp.
+#define TR_INIT                                                                                  \
+  long long* const tr_buf =                                                                      \
+      (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_trace : nullptr
 #define TR(role, blk, ev)                                                                        \
   do {                                                                                           \
-    if (g_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (blk) < TR_MAXB &&  \
-        (threadIdx.x & 31) == 0)                                                                 \
-      g_trace[((role) * TR_MAXB + (blk)) * TR_EV + (ev)] = clock64();                            \
+    if (tr_buf && (blk) < TR_MAXB && (threadIdx.x & 31) == 0)                                    \
+      tr_buf[((role) * TR_MAXB + (blk)) * TR_EV + (ev)] = clock64();                             \
   } while (0)
 #else
+#define TR_INIT \
+  do {          \
+  } while (0)
 #define TR(role, blk, ev) \
   do {                    \
   } while (0)
