@@ -42,10 +42,11 @@
 
 namespace la2 {
 
-constexpr int TC_THREADS = 480;  // 15 warps
+constexpr int TC_THREADS = 512;  // 16 warps: 4 per SM sub-partition, 128 registers each
 constexpr int NROW = 8;         // row warps (2 per TMEM lane quarter)
 constexpr int W0 = 2 + NROW;    // first state warp (4 state warps)
 constexpr int WY = W0 + 4;      // second MMA issuer (state chain)
+constexpr int WC = WY + 1;      // V~ copy warp
 
 template <int DK, bool SO>
 struct TcLayout {
@@ -75,6 +76,12 @@ struct TcLayout {
   // | Oe @320 | dKV[2] @384,448 -- S_{i+2} then only waits for PV_i, not for the epilogue.
   // State-only: dKV[2] @0,64.
   static constexpr bool OIS = (DK == 128);
+  // d = 128 (full passes): the V~ copy runs on its own warp, overlapping the state update
+  // (-10 % at C3). d = 64 keeps it in the state warps: there the kernel is close to
+  // issue-bound and a 16th busy warp slows its sub-partition (+8 %). State-only passes
+  // must keep it in the state warps: their FULL waits would otherwise let the producer
+  // run a full ring ahead of them.
+  static constexpr bool CW = (DK == 128) && !SO;
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
   static constexpr uint32_t T_O = 256, T_OE = OIS ? 256 : 320, T_KV = SO ? 0 : 384;
   // barrier slots
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&bars[L::B_OEMPTY + b], NROW);
     }
     for (int b = 0; b < KTS; ++b) {
-      mbar_init(&bars[L::B_KTREADY + b], 4);
+      mbar_init(&bars[L::B_KTREADY + b], L::CW ? 1 : 4);  // copy warp / state warps
       mbar_init(&bars[L::B_KTFREE + b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -678,21 +685,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int j = 0; j <= T; ++j) {
       if (j < T) {
-        // ---- K~(j): scaled copy of the V rows (the fold operand)
+        // record j (and stage j) is published; FULL cannot run a phase ahead of block j
+        // before U(j-1) below (or, state-only, this warp's V~ copy of block j) completes
         const int s = j % NS, kt = j % KTS;
         if (warp == W0) TR(3, j, 0);
         mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
-        const BlkRec rc = recs[j & 7];
-        const int r = min(BT, N - rc.blk * BT);
-        const float c = REV ? lam_pow(rc.l2, row + 1) : (row < r ? lam_pow(rc.l2, r - 1 - row) : 0.f);
-        if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
-        if (warp == W0) TR(3, j, 1);
-        scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
-                           row, c);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[L::B_KTREADY + kt]);
-        if (warp == W0) TR(3, j, 2);
+        if (!L::CW) {
+          // ---- K~(j): scaled copy of the V rows (the fold operand)
+          const BlkRec rc = recs[j & 7];
+          const int r = min(BT, N - rc.blk * BT);
+          const float c = REV ? lam_pow(rc.l2, row + 1) : (row < r ? lam_pow(rc.l2, r - 1 - row) : 0.f);
+          if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
+          if (warp == W0) TR(3, j, 1);
+          scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
+                             row, c);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[L::B_KTREADY + kt]);
+          if (warp == W0) TR(3, j, 2);
+        }
       }
       if (j >= 1) {
         // ---- U(j-1): KV <- lam^r KV + dKV
@@ -739,6 +750,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (warp == W0) TR(3, i, 5);
       }
+    }
+  } else if (warp == WC && L::CW) {
+    // ------------------------------------------------------------- V~ copy warp
+    // V~_j = c . V_j (c_t = lam^(r-1-t), rev: lam^(t+1)), the fold operand of dKV_j. Off
+    // the state warps, whose state update of block j-1 then overlaps this copy.
+    for (int j = 0; j < T; ++j) {
+      const int s = j % NS, kt = j % KTS;
+      mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+      const BlkRec rc = recs[j & 7];
+      const int r = min(BT, N - rc.blk * BT);
+      if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
+#pragma unroll 1
+      for (int m = 0; m < BT / 32; ++m) {
+        const int row = m * 32 + lane;
+        const float c = REV ? lam_pow(rc.l2, row + 1) : (row < r ? lam_pow(rc.l2, r - 1 - row) : 0.f);
+        scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES, row, c);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[L::B_KTREADY + kt]);
     }
   }
   tc_fence_before();
