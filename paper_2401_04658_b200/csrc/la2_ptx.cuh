@@ -36,7 +36,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+#ifndef LA2_MBAR_HINT
+#define LA2_MBAR_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if LA2_MBAR_HINT > 0
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAIT:\n\t"
@@ -44,8 +48,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@p bra.uni DONE;\n\t"
       "bra.uni LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680)
+      "r"(parity), "r"(LA2_MBAR_HINT)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra.uni DONE;\n\t"
+      "bra.uni LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // Non-blocking probe: has the phase with this parity completed?
