@@ -102,6 +102,15 @@ class ClockSampler:
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
             get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 nv.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def power_violation_ns():
+                try:
+                    return nv.nvmlDeviceGetViolationStatus(h, nv.NVML_PERF_POLICY_POWER).violationTime
+                except Exception:
+                    return None
+
+            self._viol0 = power_violation_ns()
+            self._viol_fn = power_violation_ns
             while not self._stop.is_set():
                 self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), get_reasons(h),
                                      nv.nvmlDeviceGetUtilizationRates(h).gpu))
@@ -115,9 +124,19 @@ class ClockSampler:
             self._t.join(timeout=10)
         busy = [s for s in self.samples if s[2] > 0] or self.samples
         reasons = sorted({name for s in busy for bit, name in self.REASONS.items() if s[1] & bit})
+        # NVML's power-violation counter catches SW power capping shorter than the 20 ms
+        # sampling period (sustained HBM-heavy load trips it while SM clocks read max)
+        cap_ms = None
+        v0, fn = getattr(self, "_viol0", None), getattr(self, "_viol_fn", None)
+        if v0 is not None and fn is not None:
+            v1 = fn()
+            if v1 is not None:
+                cap_ms = (v1 - v0) / 1e6
+                if cap_ms > 0 and "sw_power_cap" not in reasons:
+                    reasons = sorted(reasons + ["sw_power_cap"])
         return {"sm_mhz": statistics.median([s[0] for s in busy]) if busy else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
-                "source": "nvml"}
+                "power_cap_ms": cap_ms, "source": "nvml"}
 
 
 # ------------------------------------------------------------------ CPU side

@@ -47,6 +47,12 @@ constexpr int NROW = 8;         // row warps (2 per TMEM lane quarter)
 constexpr int W0 = 2 + NROW;    // first state warp (4 state warps)
 constexpr int WY = W0 + 4;      // second MMA issuer (state chain)
 constexpr int WC = WY + 1;      // V~ copy warp
+#ifndef LA2_GROUP_WAIT
+#define LA2_GROUP_WAIT 0
+#endif
+// Group waits: one warp of a group polls an mbarrier, its partners sleep in a named
+// barrier (fewer spinning warps: less issue pressure and power, one more bar.sync).
+constexpr bool GW = (LA2_GROUP_WAIT != 0);
 
 template <int DK, bool SO>
 struct TcLayout {
@@ -482,7 +488,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (j < T) {
           // ---- A(j): S -> P (bf16). This warp reads score columns [64h, 64h+64) and
           // writes the packed P pairs into columns [64h, 64h+32) of the same buffer.
-          mbar_wait(&bars[L::B_FULL + j % NS], (j / NS) & 1);  // record j is published
+          if (GW) {  // record j published and S_j complete: polled by half 0 only
+            if (half == 0) {
+              mbar_wait(&bars[L::B_FULL + j % NS], (j / NS) & 1);
+              mbar_wait(&bars[L::B_SFULL + (j & 1)], (j >> 1) & 1);
+            }
+            named_bar_sync(1 + q4, 64);
+          } else {
+            mbar_wait(&bars[L::B_FULL + j % NS], (j / NS) & 1);  // record j is published
+          }
           const BlkRec rc = recs[j & 7];
           if (rc.h != mask_h) {
             mask_h = rc.h;
@@ -507,7 +521,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int b = j & 1;
           const uint32_t tS = tbase + b * 128 + half * 64 + lane_off;
           if (warp == 2) TR(2, j, 0);
-          mbar_wait(&bars[L::B_SFULL + b], (j >> 1) & 1);
+          if (!GW) mbar_wait(&bars[L::B_SFULL + b], (j >> 1) & 1);
           if (warp == 2) TR(2, j, 1);
           tc_fence_after();
           // 64 score columns -> 32 packed P columns at [32h, 32h+32): P ends up contiguous
@@ -554,12 +568,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* sO = smem + L::OFF_O + (i % OS) * L::O_BYTES;
           const bool storer = (half == 0 && lane == 0);
           if (warp == 2) TR(2, i, 3);
-          if (storer) tma_store_wait_read<OS - 1>();
-          named_bar_sync(1 + q4, 64);  // the two warps of this quarter
-          if (warp == 2) TR(2, i, 4);
           const int ob = i & 1;
-          mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
-          mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
+          if (GW) {
+            if (half == 0) {
+              if (storer) tma_store_wait_read<OS - 1>();
+              mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
+              mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
+            }
+            named_bar_sync(1 + q4, 64);
+          } else {
+            if (storer) tma_store_wait_read<OS - 1>();
+            named_bar_sync(1 + q4, 64);  // the two warps of this quarter
+            if (warp == 2) TR(2, i, 4);
+            mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
+            mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
+          }
           if (warp == 2) TR(2, i, 5);
           tc_fence_after();
           float o16[2][16], e16[2][16];
@@ -716,7 +739,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const float fr = lam_pow(up_l2, static_cast<float>(r));
         if (warp == W0) TR(3, i, 3);
         const int db = i & 1;
-        mbar_wait(&bars[L::B_DKVFULL + db], (i >> 1) & 1);
+        if (!GW || warp == W0) mbar_wait(&bars[L::B_DKVFULL + db], (i >> 1) & 1);
+        if (GW) named_bar_sync(5, 128);
         if (warp == W0) TR(3, i, 4);
         tc_fence_after();
 #pragma unroll
@@ -739,7 +763,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (!SO) {
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
-          mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
+          if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
+          if (GW) named_bar_sync(5, 128);
           if (has_kv) {
 #pragma unroll
             for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
