@@ -454,6 +454,13 @@ def extra_workload(args, world, rank, local_rank):
                 "frac_of_roof": max((ff + fb) * B * H / (tc_peak * 1e12), (bf + bb) * B * H / (hbm_peak * 1e9)) * 1e3 / ms}
             q.grad = k.grad = v.grad = None
             del q, k, v, do
+        if w == "c1" and rank == 0 and not args.no_cpu:
+            # the C1 shape on the host, single core (the reference README
+            # methodology) and on all cores, beside the GPU rows
+            t_one = statistics.median([_cpu_head_task((N, D, 2000 + r, decay[r % H])) for r in range(3)])
+            cb = cpu_reference(N, D, B * H, B * N, B * H)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["single_core_tokens_per_s"] = B * N / (t_one * B * H)
         main_dt = "bfloat16" if "bfloat16" in results else "float32"
         line.update({"metric": f"{w} fwd+bwd tokens/s", "value": results[main_dt]["tokens_per_s"],
                      "unit": UNIT, "ms_per_step": results[main_dt]["ms_per_step"],
