@@ -136,6 +136,10 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *                        scan and the dK/dV pair concurrently on disjoint SM partitions
  *                        (1/3 : 2/3, both persistent); 0 disables (then the
  *                        LA2_TUNE_CONCURRENT_BWD rule applies).
+ *   LA2_TUNE_PDL         sequences with N <= value (default 4096) launch the tensor-core
+ *                        kernels with programmatic dependent launch (the prologue overlaps
+ *                        the previous kernel's tail; all global accesses wait for it);
+ *                        0: plain stream order.
  */
 #define LA2_TUNE_PERSISTENT 1
 #define LA2_TUNE_PREFETCH 2
@@ -143,6 +147,7 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
 #define LA2_TUNE_FUSED_BWD 4
 #define LA2_TUNE_CONCURRENT_BWD 5
 #define LA2_TUNE_PARTITION_BWD 6
+#define LA2_TUNE_PDL 7
 LA2_API int la2_set_tuning(int key, int value);
 
 /*

@@ -192,6 +192,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (!SO) tma_prefetch_desc(mo);
   }
   if (warp == 1) tmem_alloc(tmem_slot, L::TMEM_COLS);
+  if (threadIdx.x == 0) {
+    // Programmatic dependent launch: the prologue above overlapped the previous kernel's
+    // tail; nothing below touches global memory before that kernel has completed. Our
+    // own dependents may start their prologue now (they wait for us the same way).
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   tc_fence_before();
   if (CL) cluster_sync();  // barriers initialised in both CTAs before any remote traffic
   else __syncthreads();
@@ -867,7 +874,11 @@ static int g_persistent = env_int("LA2_NO_PERSIST", 0) ? 0 : 1;
 static int g_prefetch = env_int("LA2_PF", 0);
 static int g_l2hint = env_int("LA2_HINT", 0);
 static int g_quad = env_int("LA2_NO_QUAD", 0) ? 0 : 1;
+static int g_pdl = env_int("LA2_PDL", 4096);
 static bool persistent_enabled() { return g_persistent != 0; }
+// PDL pays only for short launches (fill/drain dominated): +2-6 % up to N = 4K, but
+// -3-7 % for long ones (measured, tools/pdl_ab.py)
+static bool pdl_enabled(int N) { return N <= g_pdl; }
 static bool quad_enabled() { return g_quad != 0; }
 static int prefetch_blocks() { return g_prefetch; }
 static int l2_hints() { return g_l2hint; }
@@ -881,6 +892,7 @@ int tuning_value(int key) {
     case LA2_TUNE_FUSED_BWD: return g_quad;
     case LA2_TUNE_CONCURRENT_BWD: return g_concurrent_bwd;
     case LA2_TUNE_PARTITION_BWD: return g_partition_bwd;
+    case LA2_TUNE_PDL: return g_pdl;
     default: return 0;
   }
 }
@@ -888,6 +900,7 @@ int set_tuning(int key, int value) {
   switch (key) {
     case LA2_TUNE_CONCURRENT_BWD: g_concurrent_bwd = value; return 0;
     case LA2_TUNE_PARTITION_BWD: g_partition_bwd = value; return 0;
+    case LA2_TUNE_PDL: g_pdl = value; return 0;
     case LA2_TUNE_PERSISTENT: g_persistent = value; return 0;
     case LA2_TUNE_PREFETCH: g_prefetch = value; return 0;
     case LA2_TUNE_L2HINT: g_l2hint = value; return 0;
@@ -951,13 +964,22 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int nattr = 0;
+  if (CM) {
+    attr[nattr].id = cudaLaunchAttributeClusterDimension;
+    attr[nattr].val.clusterDim.x = CS;
+    attr[nattr].val.clusterDim.y = 1;
+    attr[nattr].val.clusterDim.z = 1;
+    ++nattr;
+  }
+  if (pdl_enabled(a.N)) {
+    attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+    ++nattr;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = CM ? 1 : 0;
+  cfg.numAttrs = CM ? 1 : 0;  // cluster only, for the occupancy query below
   if (persistent_enabled()) {
     // co-resident work ranges (one CTA per SM: smem and TMEM are sized for it)
     static int max_ranges = -1;
@@ -988,6 +1010,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     }
   }
   cfg.gridDim = dim3(p.P * CS);
+  cfg.numAttrs = nattr;
   e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mk1, mv1, mo1, p);
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   e = cudaGetLastError();

@@ -226,7 +226,7 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     return dq, dk, dvv, dkv_out
 
 
-TUNE_PERSISTENT, TUNE_PREFETCH, TUNE_L2HINT, TUNE_FUSED_BWD, TUNE_CONCURRENT_BWD, TUNE_PARTITION_BWD = 1, 2, 3, 4, 5, 6
+TUNE_PERSISTENT, TUNE_PREFETCH, TUNE_L2HINT, TUNE_FUSED_BWD, TUNE_CONCURRENT_BWD, TUNE_PARTITION_BWD, TUNE_PDL = 1, 2, 3, 4, 5, 6, 7
 
 
 def set_tuning(key: int, value: int) -> None:
