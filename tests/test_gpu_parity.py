@@ -583,3 +583,28 @@ def test_random_shapes_against_oracle(case):
     rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
     errs = {"o": rel(o, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
     assert max(errs.values()) <= BF16_TOL, ((B, H, N, d, dv), errs)
+
+
+def test_fused_g_backward_opt_in():
+    """The single-CTA fused dK/dV scan (la2_bwd.cu, opt-in with LA2_FUSED_BWD_G; slower than
+    the cluster pair) still matches the oracle -- run in a subprocess so the env applies."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = (
+        "import numpy as np, torch, paper_2401_04658_b200 as la2\n"
+        "from oracle import tila_port as port\n"
+        "g = torch.Generator().manual_seed(4)\n"
+        "q, k, v, do = ((torch.rand(2, 3, 700, 64, generator=g) * 2 - 1).bfloat16() for _ in range(4))\n"
+        "decay = [0.9, 0.999, 1.0]\n"
+        "dq, dk, dv, _ = la2.la2_backward(*(t.cuda() for t in (q, k, v, do)), decay)\n"
+        "Q, K, V, DO = (t.double().numpy() for t in (q, k, v, do))\n"
+        "rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)\n"
+        "e = max(port.rel_err(a.double().cpu().numpy(), b) for a, b in ((dq, rq), (dk, rk), (dv, rv)))\n"
+        "assert e <= 1e-2, e\n"
+        "print('ok', e)\n")
+    root = Path(__file__).resolve().parents[1]
+    env = dict(__import__("os").environ, LA2_FUSED_BWD_G="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
