@@ -487,9 +487,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
       // Mask factors for this row and this warp's 4 chunks of 16 score columns:
       //   M[row][16ch + j] = (ch == dch) ? Dg[j] : F[ch] * G[j]   (F = 0 on the zero side)
-      // recomputed whenever the schedule moves to another head.
-      float G[16], Dg[16], F[4];
+      // recomputed whenever the schedule moves to another head. Each 32-column half hh of
+      // the warp's columns is, for all 32 rows of the warp, either entirely masked out
+      // (kind 0: no TMEM load, zeros), entirely decayed (kind 1: F[c] * G[j]), or it
+      // straddles the diagonal (kind 2, only when 2*half + hh == q4: per-lane factors MX
+      // precomputed with the head). Warp-uniform, so no divergence and no per-element
+      // selects on the hot path.
+      float G[16], F[4], MX[2][16];
       const int dch = row >> 4, tt = row & 15;
+      const int hm = q4 - 2 * half;  // the straddling half (0/1) or none
+      const int kind0 = (2 * half == q4) ? 2 : ((REV ? 2 * half > q4 : 2 * half < q4) ? 1 : 0);
+      const int kind1 = (2 * half + 1 == q4) ? 2 : ((REV ? 2 * half + 1 > q4 : 2 * half + 1 < q4) ? 1 : 0);
       int mask_h = -1;
       for (int j = 0; j <= T; ++j) {
         if (j < T) {
@@ -509,20 +517,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mask_h = rc.h;
             const float l2 = rc.l2;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              if (!REV) {
-                G[jj] = lam_pow(l2, 15 - jj);
-                Dg[jj] = (jj <= tt) ? lam_pow(l2, tt - jj) : 0.f;
-              } else {
-                G[jj] = lam_pow(l2, jj);
-                Dg[jj] = (jj >= tt) ? lam_pow(l2, jj - tt) : 0.f;
-              }
-            }
+            for (int jj = 0; jj < 16; ++jj) G[jj] = REV ? lam_pow(l2, jj) : lam_pow(l2, 15 - jj);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int ch = 4 * half + c;
               if (!REV) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
               else F[c] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
+            }
+            if (hm == 0 || hm == 1) {
+#pragma unroll
+              for (int cc = 0; cc < 2; ++cc) {
+                const int ch = 4 * half + 2 * hm + cc;
+                const float fv = !REV ? ((ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f)
+                                      : ((ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f);
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  const float dg = !REV ? ((jj <= tt) ? lam_pow(l2, tt - jj) : 0.f)
+                                        : ((jj >= tt) ? lam_pow(l2, jj - tt) : 0.f);
+                  MX[cc][jj] = (ch == dch) ? dg : fv * G[jj];
+                }
+              }
             }
           }
           const int b = j & 1;
@@ -538,16 +552,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint32_t pk[2][16];
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            uint32_t raw[32];
-            tmem_ld32_raw(tS + hh * 32, raw);
-            tmem_ld_wait();
+            const int kd = hh ? kind1 : kind0;
+            if (kd == 0) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int c = 2 * hh + (e >> 3), ch = 4 * half + c, jj = (2 * e) & 15;
-              const float m0 = (ch == dch) ? Dg[jj] : F[c] * G[jj];
-              const float m1 = (ch == dch) ? Dg[jj + 1] : F[c] * G[jj + 1];
-              pk[hh][e] = pack_bf16x2(__uint_as_float(raw[2 * e]) * m0,
-                                      __uint_as_float(raw[2 * e + 1]) * m1);
+              for (int e = 0; e < 16; ++e) pk[hh][e] = 0u;
+            } else {
+              uint32_t raw[32];
+              tmem_ld32_raw(tS + hh * 32, raw);
+              tmem_ld_wait();
+              if (kd == 1) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const int c = 2 * hh + (e >> 3), jj = (2 * e) & 15;
+                  const float2 m = __fmul2_rn(make_float2(G[jj], G[jj + 1]), make_float2(F[c], F[c]));
+                  const float2 x = __fmul2_rn(make_float2(__uint_as_float(raw[2 * e]),
+                                                          __uint_as_float(raw[2 * e + 1])), m);
+                  pk[hh][e] = pack_bf16x2(x.x, x.y);
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const int cc = e >> 3, jj = (2 * e) & 15;
+                  const float2 x = __fmul2_rn(make_float2(__uint_as_float(raw[2 * e]),
+                                                          __uint_as_float(raw[2 * e + 1])),
+                                              make_float2(MX[cc][jj], MX[cc][jj + 1]));
+                  pk[hh][e] = pack_bf16x2(x.x, x.y);
+                }
+              }
             }
             if (!L::OIS) tmem_st16(tS + hh * 16, pk[hh]);  // in place: no cross-warp hazard
           }
@@ -609,7 +640,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) o16[q][e] = fmaf(a, e16[q][e], o16[q][e]);
+            for (int e = 0; e < 16; e += 2) {
+              const float2 y = __ffma2_rn(make_float2(e16[q][e], e16[q][e + 1]), make_float2(a, a),
+                                          make_float2(o16[q][e], o16[q][e + 1]));
+              o16[q][e] = y.x;
+              o16[q][e + 1] = y.y;
+            }
             store_chunk16_bf16(sO, row, 2 * half + q, o16[q]);
           }
           fence_proxy_async_smem();
@@ -757,12 +793,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) kv[32 * q + e] = fmaf(fr, kv[32 * q + e], __uint_as_float(d32[e]));
+            for (int e = 0; e < 32; e += 2) {
+              const float2 y = __ffma2_rn(make_float2(kv[32 * q + e], kv[32 * q + e + 1]), make_float2(fr, fr),
+                                          make_float2(__uint_as_float(d32[e]), __uint_as_float(d32[e + 1])));
+              kv[32 * q + e] = y.x;
+              kv[32 * q + e + 1] = y.y;
+            }
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[L::B_DKVEMPTY + db]);
+        if (warp == W0) TR(3, i, 6);
         if (flags & REC_SEG_END) store_state(bh, slice, pos);
         if (j < T) {
           const BlkRec rn = recs[j & 7];  // acquired in K~(j) above
@@ -772,6 +814,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
           if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (GW) named_bar_sync(5, 128);
+          if (warp == W0) TR(3, i, 7);
           if (has_kv) {
 #pragma unroll
             for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);

@@ -49,8 +49,8 @@ __device__ __forceinline__ void scale_row_copy(const uint8_t* src, uint8_t* dst,
       uint32_t* u = reinterpret_cast<uint32_t*>(&w[k]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        float2 x = unpack_bf16x2(u[e]);
-        u[e] = pack_bf16x2(x.x * f, x.y * f);
+        const float2 x = __fmul2_rn(unpack_bf16x2(u[e]), make_float2(f, f));
+        u[e] = pack_bf16x2(x.x, x.y);
       }
       // chunks are rotated by row to spread banks across the warp
       *reinterpret_cast<uint4*>(dp + ((k + row) & 7) * 16) = w[k];

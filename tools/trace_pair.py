@@ -26,7 +26,7 @@ t = buf.cpu().numpy().reshape(4, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, -1)
 names = {0: "TMA  [pre-wait, loads]", 1: "MMA  [iter, S(i+1) issued, PREADY, OEMPTY, KVREADY, KT/DKVEMPTY, end]",
-         2: "ROW  [A start, S ready, A end, B start, stbar, OFULL, B end]", 3: "STATE[K~ start, K ready, K~ end, U start, DKVFULL, U end]"}
+         2: "ROW  [A start, S ready, A end, B start, stbar, OFULL, B end]", 3: "STATE[K~ start, K ready, K~ end, U start, DKVFULL, U end, dkv loaded, OEFULL]"}
 for role in range(4):
     print(names[role])
     for i in list(range(0, 4)) + list(range(40, 46)):
