@@ -57,6 +57,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Pa
     if not trace and not force and not _stale():
         return LIB
     extra, tag = (["-DLA2_TRACE"], "_trace") if trace else ((), "")
+    extra = [*extra, *os.environ.get("LA2_NVCC_EXTRA", "").split()]
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose, extra, tag), SOURCES))
     tmp = lib.with_suffix(".so.tmp")

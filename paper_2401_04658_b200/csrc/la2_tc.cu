@@ -541,9 +541,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           const int b = j & 1;
           const uint32_t tS = tbase + b * 128 + half * 64 + lane_off;
-          if (warp == 2) TR(2, j, 0);
+          if (warp == LA2_TRW) TR(2, j, 0);
           if (!GW) mbar_wait(&bars[L::B_SFULL + b], (j >> 1) & 1);
-          if (warp == 2) TR(2, j, 1);
+          if (warp == LA2_TRW) TR(2, j, 1);
           tc_fence_after();
           // 64 score columns -> 32 packed P columns at [32h, 32h+32): P ends up contiguous
           // in columns 0..63 of S[b] and columns 64..127 are free for O_i = P_i V_i. The
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[L::B_PREADY + b]);
-          if (warp == 2) TR(2, j, 2);
+          if (warp == LA2_TRW) TR(2, j, 2);
         }
         if (j >= 1) {
           // ---- B(j-1): o = O + a_t Oe for value columns [32h, 32h+32) -> smem -> TMA store
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const float a = REV ? (row < r ? lam_pow(out_l2, r - 1 - row) : 0.f) : lam_pow(out_l2, row + 1);
           uint8_t* sO = smem + L::OFF_O + (i % OS) * L::O_BYTES;
           const bool storer = (half == 0 && lane == 0);
-          if (warp == 2) TR(2, i, 3);
+          if (warp == LA2_TRW) TR(2, i, 3);
           const int ob = i & 1;
           if (GW) {
             if (half == 0) {
@@ -617,11 +617,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           } else {
             if (storer) tma_store_wait_read<OS - 1>();
             named_bar_sync(1 + q4, 64);  // the two warps of this quarter
-            if (warp == 2) TR(2, i, 4);
+            if (warp == LA2_TRW) TR(2, i, 4);
             mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
             mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
           }
-          if (warp == 2) TR(2, i, 5);
+          if (warp == LA2_TRW) TR(2, i, 5);
           tc_fence_after();
           float o16[2][16], e16[2][16];
 #pragma unroll
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_store_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
             tma_store_commit();
           }
-          if (warp == 2) TR(2, i, 6);
+          if (warp == LA2_TRW) TR(2, i, 6);
         }
       }
       if (half == 0 && lane == 0) tma_store_wait_all0();

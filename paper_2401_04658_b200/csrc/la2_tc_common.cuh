@@ -8,6 +8,9 @@ namespace la2 {
 
 // Optional phase trace (build with -DLA2_TRACE): CTA (0,0,0) records clock64()
 // stamps per role / block / event into g_trace[role][block][event].
+#ifndef LA2_TRW
+#define LA2_TRW 2  // the row warp whose phases are traced
+#endif
 #ifdef LA2_TRACE
 static __device__ long long* g_trace = nullptr;  // per translation unit
 constexpr int TR_MAXB = 64, TR_EV = 8;  // roles 0..4
