@@ -11,6 +11,7 @@ Public API
   decode_step                           recurrent decode (tila.inference_step)
   sp_lightning_attn2                    sequence parallel over torch.distributed
   tila_api                              the reference's numpy operator API on the GPU
+  matrix                                seeded inputs and text fixtures (tila.matrix)
 """
 
 from .ops import (

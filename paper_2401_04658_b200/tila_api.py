@@ -10,6 +10,8 @@ run unchanged against this module:
   batched_forward(inputs, block, parallel)      pkg/src/tila/kernel.py:252-260
   batched_backward(inputs, block, parallel)     pkg/src/tila/kernel.py:263-266
   inference_step(q_t, k_t, v_t, state, lam)     pkg/src/tila/reference.py:162-181
+  random_matrix, save_fixture, load_fixture,    pkg/src/tila/matrix.py (re-exported from
+  AttentionConfig, FixtureFormatError           ``matrix``: seeded inputs, text fixtures)
 
 Inputs and outputs are 2-D NumPy arrays (one head), like the reference. The
 arithmetic runs on the GPU in fp32 (the north star's fp32 path, tolerance
@@ -28,6 +30,16 @@ import numpy as np
 import torch
 
 from . import ops
+from .matrix import (  # noqa: F401  (re-exported: the reference's top-level namespace)
+    PRECISIONS,
+    AttentionConfig,
+    FixtureFormatError,
+    dtype_for,
+    load_fixture,
+    precision_of,
+    random_matrix,
+    save_fixture,
+)
 
 _FLOATS = (np.dtype(np.float32), np.dtype(np.float64))
 

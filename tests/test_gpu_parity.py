@@ -316,6 +316,27 @@ def test_tila_api_batched_per_head_decay():
         assert port.rel_err(r.o, port.oracle_forward(q, k, v, lam)) <= FP32_TOL
 
 
+def test_tila_api_text_fixtures(tmp_path):
+    """Golden vectors shipped as text fixtures (tila.matrix format): written with the
+    reference's seeds, read back, run through the GPU, results written and re-read."""
+    n, d, dv, lam = 300, 16, 19, 0.97
+    names = ("q", "k", "v", "d_out")
+    for i, (nm, cols) in enumerate(zip(names, (d, d, dv, dv))):
+        tila_api.save_fixture(tila_api.random_matrix(n, cols, 70 + i, "single"), tmp_path / f"{nm}.txt")
+    q, k, v, d_out = (tila_api.load_fixture(tmp_path / f"{nm}.txt") for nm in names)
+    assert q.dtype == np.float32
+    res = tila_api.tiled_forward(q, k, v, lam, 64)
+    g = tila_api.tiled_backward(q, k, v, d_out, lam, 64)
+    tila_api.save_fixture(res.o, tmp_path / "o.txt")
+    o = tila_api.load_fixture(tmp_path / "o.txt")
+    assert np.array_equal(o, res.o)
+    q64, k64, v64, d64 = (x.astype(np.float64) for x in (q, k, v, d_out))
+    assert port.rel_err(o, port.oracle_forward(q64, k64, v64, lam)) <= FP32_TOL
+    go = port.oracle_backward(q64, k64, v64, d64, lam)
+    for a in ("dq", "dk", "dv"):
+        assert port.rel_err(getattr(g, a), getattr(go, a)) <= FP32_TOL
+
+
 # ------------------------------------------------------------ large-N property
 def test_long_sequence_bf16():
     """BASELINE sizes: N = 65536, d = 64 against the O(n) fp64 tiled oracle,
