@@ -269,6 +269,33 @@ def test_decode_golden_and_fold(golden):
     assert rel(st, ref_kv) <= FP32_TOL * 10
 
 
+def test_prefill_decode_multitoken_stream():
+    """Serving path: prefill (la2_forward with the final state), single-token decode
+    steps, a multi-token chunk through la2_forward(kv_in=...), more decode -- the
+    concatenated outputs and the final state equal the one-shot forward."""
+    B, H, D = 2, 3, 64
+    pieces = [700, 1, 1, 1, 3, 1, 130, 1]
+    N = sum(pieces)
+    decay = [0.9, 0.999, 1.0]
+    q, k, v, _ = inputs(B, H, N, D, D, torch.bfloat16, seed=77)
+    qg, kg, vg = gpu(q, k, v)
+    ref_o, ref_kv = la2.la2_forward(qg, kg, vg, decay, output_final_state=True)
+    st, outs, t = None, [], 0
+    for L in pieces:
+        sl = slice(t, t + L)
+        if L == 1 and st is not None:
+            outs.append(la2.decode_step(qg[:, :, t], kg[:, :, t], vg[:, :, t], decay, st).unsqueeze(2))
+        else:
+            o, st = la2.la2_forward(qg[:, :, sl].contiguous(), kg[:, :, sl].contiguous(),
+                                    vg[:, :, sl].contiguous(), decay, kv_in=st, output_final_state=True)
+            outs.append(o)
+        t += L
+    assert rel(torch.cat(outs, 2), to64(ref_o)) <= BF16_TOL
+    assert rel(st, to64(ref_kv)) <= FP32_TOL * 10
+    po, pkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay)
+    assert rel(torch.cat(outs, 2), po) <= BF16_TOL and rel(st, pkv) <= BF16_TOL
+
+
 # ------------------------------------------------------------- tila mirror API
 def test_tila_api_kats():
     ones = [[1.0], [1.0]]
