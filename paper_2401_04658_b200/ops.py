@@ -120,7 +120,9 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     reshape) gives G x more units at the cost of one state-only pass over K,V (and
     Q,dO in the backward). Tensor-core path: used when units < ~100 and chunks stay
     >= 2048 tokens. SIMT path (fp32 / other shapes, several CTAs per SM): split until
-    ~4 units per SM with chunks >= 256 tokens.
+    ~4 units per SM, down to 32-token chunks at d <= 64 (128 above), at most 64 chunks
+    (the state scan's limit). Measured on B200 (tools/fp32_split.py): C1 fp32 fwd+bwd
+    1.22 ms at 8 chunks -> 0.53 ms at 64.
     """
     units = B * H * ((dv + 63) // 64)
     g = 1
@@ -132,7 +134,8 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
         return g
     if d > 256 or dv > 256:
         return 1
-    while units * g < 4 * NUM_SMS and N % (2 * g) == 0 and N // (2 * g) >= 256:
+    min_chunk = 32 if max(d, dv) <= 64 else 128
+    while units * g < 4 * NUM_SMS and 2 * g <= 64 and N % (2 * g) == 0 and N // (2 * g) >= min_chunk:
         g *= 2
     return g
 
