@@ -118,8 +118,10 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     One CTA owns one (b, h, 64-wide value slice) for the whole sequence, so with
     fewer units than SMs the GPU idles. Viewing [B,H,N,d] as [B,H*G,N/G,d] (a free
     reshape) gives G x more units at the cost of one state-only pass over K,V (and
-    Q,dO in the backward). Tensor-core path: used when units < ~100 and chunks stay
-    >= 2048 tokens. SIMT path (fp32 / other shapes, several CTAs per SM): split until
+    Q,dO in the backward). Tensor-core path: used when units < ~100, chunks stay
+    >= 8192 tokens and the split is at least 4-way (measured: at B=1, H=8, N=8192 the
+    unsplit fwd+bwd takes 0.20 ms and every split 0.33-0.37 ms; at H=16, N=16384 splits
+    are within noise of no split; at H=4, N=64K an 8-way split is 4.7x faster). SIMT path (fp32 / other shapes, several CTAs per SM): split until
     ~4 units per SM, down to 32-token chunks at d <= 64 (128 above), at most 64 chunks
     (the state scan's limit). Measured on B200 (tools/fp32_split.py): C1 fp32 fwd+bwd
     1.22 ms at 8 chunks -> 0.53 ms at 64.
@@ -129,9 +131,11 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     if dtype == torch.bfloat16 and d in (64, 128) and dv % 64 == 0:
         if units >= 100:
             return 1
-        while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 2048:
+        while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 8192:
             g *= 2
-        return g
+        # each pass of a split runs over N/g tokens serially plus fixed launch/ramp costs,
+        # so a 2-way split never pays (tools/bf16_split.py)
+        return g if g >= 4 else 1
     if d > 256 or dv > 256:
         return 1
     min_chunk = 32 if max(d, dv) <= 64 else 128

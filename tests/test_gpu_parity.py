@@ -423,7 +423,7 @@ def test_sequence_split_matches_reference(g, d):
 
 def test_autograd_auto_split():
     """lightning_attn2 picks the split automatically for few heads and long N."""
-    B, H, N, D = 1, 2, 16384, 128
+    B, H, N, D = 1, 2, 32768, 128
     assert la2.split_factor(B, H, N, D, D, torch.bfloat16) > 1
     decay = [0.9999, 1.0]
     q, k, v, do = inputs(B, H, N, D, D, torch.bfloat16, seed=123)

@@ -69,13 +69,16 @@ def test_tila_api_requires_gpu():
 
 def test_split_factor_policy():
     """Intra-GPU sequence split: tensor-core shapes split only when units underfill the
-    GPU (chunks >= 2048 tokens); SIMT shapes (fp32) split to ~4 units per SM (chunks >= 32
+    GPU (chunks >= 8192 tokens, at least 4-way); SIMT shapes (fp32) split to ~4 units per SM (chunks >= 32
     tokens at d <= 64, >= 128 above; at most 64 chunks)."""
     import torch
     from paper_2401_04658_b200.ops import split_factor
     assert split_factor(8, 16, 65536, 64, 64, torch.bfloat16) == 1        # C2: 128 units
     assert split_factor(1, 16, 524288, 128, 128, torch.bfloat16) == 8     # C5 on one GPU
     assert split_factor(1, 2, 300, 64, 64, torch.bfloat16) == 1           # too short
+    assert split_factor(1, 8, 8192, 64, 64, torch.bfloat16) == 1          # 2-way never pays
+    assert split_factor(1, 16, 16384, 64, 64, torch.bfloat16) == 1        # chunks < 8192 tokens
+    assert split_factor(1, 4, 65536, 64, 64, torch.bfloat16) == 8
     assert split_factor(1, 8, 2048, 64, 64, torch.float32) == 64          # C1 fp32 (SIMT)
     assert split_factor(1, 8, 1024, 64, 64, torch.float32) == 32          # 32-token chunks
     assert split_factor(1, 8, 2048, 128, 128, torch.float32) == 16        # d=128: >= 128 tokens
