@@ -77,6 +77,31 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
     return torch.tensor(vals, dtype=torch.float32, device=device)
 
 
+_DECAY_CACHE: dict = {}
+
+
+def _decay(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
+    """decay_tensor for the ops' own use: host values (lists, floats, CPU tensors) are
+    validated and uploaded once per distinct (values, device) and the device copy is
+    reused -- a fresh upload costs ~16 us of host time per call. The cached tensor is
+    never handed to the caller (only read by the kernels)."""
+    if isinstance(decay, torch.Tensor) and decay.is_cuda:
+        return decay_tensor(decay, H, device)
+    if isinstance(decay, (int, float)):
+        key = ((float(decay),), H, device)
+    elif isinstance(decay, torch.Tensor):
+        key = (tuple(decay.detach().double().reshape(-1).tolist()), H, device)
+    else:
+        key = (tuple(float(x) for x in decay), H, device)
+    t = _DECAY_CACHE.get(key)
+    if t is None:
+        t = decay_tensor(list(key[0]), H, device)
+        if len(_DECAY_CACHE) >= 256:
+            _DECAY_CACHE.clear()
+        _DECAY_CACHE[key] = t
+    return t
+
+
 def _check_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     qs, vs = q.shape, v.shape
     if (len(qs) == 4 and k.shape == qs and len(vs) == 4 and vs[:3] == qs[:3] and q.is_cuda
@@ -164,7 +189,7 @@ def split_forward(q, k, v, decay, g: int, kv_in=None, output_final_state=False):
     """Forward with the sequence cut into g chunks per (b, h). Returns
     ``(o, kv_out, prefix)``; prefix (chunk-carried states) is reused by the backward."""
     B, H, N, d, dv = _check_qkv(q, k, v)
-    dec = decay_tensor(decay, H, q.device)
+    dec = _decay(decay, H, q.device)
     dec_g = dec.repeat_interleave(g)
     q4, k4, v4 = _chunked(q.contiguous(), g), _chunked(k.contiguous(), g), _chunked(v.contiguous(), g)
     s = chunk_state(k4, v4, dec_g)
@@ -178,7 +203,7 @@ def split_forward(q, k, v, decay, g: int, kv_in=None, output_final_state=False):
 def split_backward(q, k, v, d_out, decay, g: int, prefix, dkv_in=None, output_dkv=False):
     """Backward matching :func:`split_forward` (prefix = its chunk-carried states)."""
     B, H, N, d, dv = _check_qkv(q, k, v)
-    dec = decay_tensor(decay, H, q.device)
+    dec = _decay(decay, H, q.device)
     dec_g = dec.repeat_interleave(g)
     q4, k4, v4, do4 = (_chunked(t.contiguous(), g) for t in (q, k, v, d_out))
     t = chunk_dstate(q4, do4, dec_g)
@@ -201,7 +226,7 @@ def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
     """
     B, H, N, d, dv = _check_qkv(q, k, v)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    dec = decay_tensor(decay, H, q.device)
+    dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     o = torch.empty_like(v)
     kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
@@ -222,7 +247,7 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     if d_out.shape != v.shape or d_out.dtype != v.dtype:
         raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
     q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
-    dec = decay_tensor(decay, H, q.device)
+    dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
     dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
@@ -246,7 +271,7 @@ def chunk_state(k, v, decay: DecayLike) -> torch.Tensor:
     """S = sum_s lam^(N-1-s) k_s^T v_s  (fp32 [B,H,d,dv]); sequence-parallel pass A."""
     B, H, N, d, dv = _check_qkv(k, k, v)
     k, v = k.contiguous(), v.contiguous()
-    dec = decay_tensor(decay, H, k.device)
+    dec = _decay(decay, H, k.device)
     out = torch.empty(B, H, d, dv, device=k.device, dtype=torch.float32)
     _lib.call("la2_chunk_state", _ptr(k), _ptr(v), _ptr(dec), _ptr(out), B, H, N, d, dv, _code(k),
               _stream(k.device))
@@ -257,7 +282,7 @@ def chunk_dstate(q, d_out, decay: DecayLike) -> torch.Tensor:
     """T = sum_s lam^(s+1) q_s^T d_out_s (fp32 [B,H,d,dv]); SP backward pass A."""
     B, H, N, d, dv = _check_qkv(q, q, d_out)
     q, d_out = q.contiguous(), d_out.contiguous()
-    dec = decay_tensor(decay, H, q.device)
+    dec = _decay(decay, H, q.device)
     out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32)
     _lib.call("la2_chunk_dstate", _ptr(q), _ptr(d_out), _ptr(dec), _ptr(out), B, H, N, d, dv,
               _code(q), _stream(q.device))
@@ -273,7 +298,7 @@ def state_scan(states: torch.Tensor, decay: DecayLike, lens: Sequence[int],
     if len(lens) != G:
         raise ValueError(f"lens must have {G} entries")
     states = states.contiguous()
-    dec = decay_tensor(decay, H, states.device)
+    dec = _decay(decay, H, states.device)
     if init is not None:
         init = _state(init, B, H, d, dv, states.device, "init")
     out = torch.empty_like(states)
@@ -299,7 +324,7 @@ def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.T
     if not (q_t.dtype == k_t.dtype == v_t.dtype):
         raise ValueError("q_t, k_t, v_t must share a dtype")
     q_t, k_t, v_t = q_t.contiguous(), k_t.contiguous(), v_t.contiguous()
-    dec = decay_tensor(decay, H, q_t.device)
+    dec = _decay(decay, H, q_t.device)
     o = torch.empty_like(v_t)
     _lib.call("la2_decode_step", _ptr(q_t), _ptr(k_t), _ptr(v_t), _ptr(dec), _ptr(state), _ptr(o),
               B, H, d, dv, _code(q_t), _stream(q_t.device))
@@ -361,7 +386,7 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
     Returns ``o`` (``[B,H,N,dv]``, input dtype), or ``(o, final_state)``.
     """
     _check_qkv(q, k, v)
-    dec = decay_tensor(decay, q.shape[1], q.device)
+    dec = _decay(decay, q.shape[1], q.device)
     if initial_state is not None:
         B, H, N, d = q.shape
         if tuple(initial_state.shape) != (B, H, d, v.shape[3]):

@@ -656,3 +656,17 @@ def test_fused_g_backward_opt_in():
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_host_decay_upload_cached():
+    """Host decay values (list / float / CPU tensor) are validated and uploaded once per
+    distinct value set; the public decay_tensor still returns a fresh tensor."""
+    from paper_2401_04658_b200 import ops
+    a = ops._decay([0.9, 0.5, 1.0], 3, DEV)
+    assert a is ops._decay((0.9, 0.5, 1.0), 3, DEV)
+    assert a is ops._decay(torch.tensor([0.9, 0.5, 1.0], dtype=torch.float64), 3, DEV)
+    assert ops._decay(0.7, 4, DEV) is ops._decay(0.7, 4, DEV) and ops._decay(0.7, 4, DEV).numel() == 4
+    assert la2.decay_tensor([0.9, 0.5, 1.0], 3, DEV) is not a
+    for bad in ([0.9, 1.5, 1.0], [0.0, 0.5, 0.5], [0.5, 0.5]):
+        with pytest.raises(ValueError):
+            ops._decay(bad, 3, DEV)
