@@ -23,9 +23,16 @@ tensors (the reference's single-head shape), "chunked" = STREAM_CHUNKS calls wit
 the carried fp32 state, "recurrent" = one la2_decode_step per token. The
 reference's "oracle" (O(n^2) CPU) has no GPU counterpart here.
 
+* ``acceptance_scaling``                 -- pkg/tests/test_acceptance.py:51-62, :129-144
+                                          (criterion 5: tiled fwd+bwd over n = 8K..64K at
+                                          d=64 is linear-like and the per-token time
+                                          spread max/min is <= 1.5)
+
 Run: ``python -m paper_2401_04658_b200.gpubench --csv out.csv`` (prints the
-verdicts; exit code 0 when every implementation is linear-like, like
-``tila bench``'s acceptance check).
+verdicts and the criterion-5 spread; exit code 0 when every implementation is
+linear-like and the tiled spread is <= 1.5, like the reference's acceptance check).
+The default n list is the reference's acceptance sweep; ``--n 1024,...,65536`` adds
+the short-sequence points, where fixed launch costs dominate a GPU pass.
 """
 
 from __future__ import annotations
@@ -212,6 +219,21 @@ def block_size_sweep(n: int, d: int, lam: float, blocks, reps: int = 5, seed: in
     return [time_pass("tiled", "forward", n, d, d, b, lam, reps, seed, dtype) for b in blocks]
 
 
+ACCEPTANCE_N = (8192, 16384, 32768, 65536)
+ACCEPTANCE_SPREAD = 1.5
+
+
+def acceptance_scaling(heads: int = 128, dtype=torch.bfloat16, reps: int = 5):
+    """Criterion 5 of the reference (test_acceptance.py:129-144) on the GPU path:
+    returns (records, verdict, spread, ok)."""
+    records, verdicts = scaling_sweep(["tiled"], ACCEPTANCE_N, 64, lam=0.9, reps=reps,
+                                      dtype=dtype, heads=heads)
+    per_tok = [r.per_token_microseconds for r in records]
+    spread = max(per_tok) / min(per_tok)
+    ok = verdicts[0].classification == "linear-like" and spread <= ACCEPTANCE_SPREAD
+    return records, verdicts[0], spread, ok
+
+
 def _fmt(x) -> str:
     return format(x, ".17g") if isinstance(x, float) else str(x)
 
@@ -232,7 +254,7 @@ def emit_csv(records, path) -> None:
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description="GPU scaling sweep with the reference verdict")
     ap.add_argument("--impls", default="tiled,chunked")
-    ap.add_argument("--n", default="1024,2048,4096,8192,16384,32768,65536")
+    ap.add_argument("--n", default=",".join(str(n) for n in ACCEPTANCE_N))
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--heads", type=int, default=128,
                     help="heads per call (the reference times one head; one B200 needs ~128)")
@@ -244,9 +266,16 @@ def main(argv=None) -> int:
                                       lam=a.lam, reps=a.reps, heads=a.heads)
     if a.csv:
         emit_csv(records, a.csv)
+    ok = True
     for v in verdicts:
         print(f"{v.impl}: {v.classification} (doubling ratios {', '.join(f'{r:.2f}' for r in v.ratios)})")
-    return 0 if all(v.classification == "linear-like" for v in verdicts) else 1
+        ok = ok and v.classification == "linear-like"
+        if v.impl == "tiled":
+            per_tok = [r.per_token_microseconds for r in records if r.impl == "tiled"]
+            spread = max(per_tok) / min(per_tok)
+            print(f"tiled per-token max/min {spread:.2f} (criterion 5 needs <= {ACCEPTANCE_SPREAD})")
+            ok = ok and spread <= ACCEPTANCE_SPREAD
+    return 0 if ok else 1
 
 
 if __name__ == "__main__":

@@ -583,6 +583,16 @@ def test_gpubench_sweep_and_block_invariance():
     assert [r.block for r in rows] == [16, 64, 256]
 
 
+def test_acceptance_criterion_5_on_gpu():
+    """The reference's scaling acceptance (test_acceptance.py:51-62, :129-144): tiled
+    fwd+bwd over n = 8K..64K at d = 64 is linear-like with per-token spread <= 1.5 --
+    here on the GPU path (bf16, 128 heads so one call fills the B200)."""
+    from paper_2401_04658_b200 import gpubench as gb
+    recs, verdict, spread, ok = gb.acceptance_scaling(heads=128, reps=5)
+    assert [r.n for r in recs] == list(gb.ACCEPTANCE_N)
+    assert ok, (verdict.ratios, verdict.classification, spread)
+
+
 def test_partitioned_backward_bitwise():
     """d = 64: the dQ scan and the dK/dV pair run concurrently on disjoint SM partitions
     (both persistent, capped ranges) -- gradients bitwise equal to the serial order."""

@@ -109,6 +109,9 @@ def test_gpubench_verdict_and_csv(tmp_path):
     assert lines[1] == "tiled,fwd+bwd,1024,64,64,64,0.90000000000000002,5,0.0001,0.10000000000000001,0"
     with pytest.raises(ValueError):
         gb.emit_csv([], p)
+    # criterion 5 of the reference's acceptance suite (test_acceptance.py:51-62)
+    assert gb.ACCEPTANCE_N == (8192, 16384, 32768, 65536) and gb.ACCEPTANCE_SPREAD == 1.5
+    gb._check_n_list(gb.ACCEPTANCE_N)
 
 
 def test_cli_usage_errors_exit_2():
