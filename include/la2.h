@@ -6,8 +6,11 @@
  * reference function; the citation is given per function. The ABI takes
  * plain device pointers, sizes and a cudaStream_t passed as void*; it has no
  * torch types. All launches are asynchronous on the caller's stream; the
- * library never allocates, frees or retains caller memory and keeps no hidden
- * HBM workspace.
+ * library never allocates, frees or retains caller memory. Its only own device
+ * memory is one fixed workspace per (device, stream) -- the stream-K state
+ * hand-off slots, la2_workspace_bytes() bytes (~4.7 MB on B200), allocated on the
+ * first launch on that stream outside graph capture and kept for the process
+ * lifetime; it does not grow with B, H or N.
  *
  * Layouts (all contiguous, row-major):
  *   q, k, dq, dk          [B, H, N, d]
@@ -149,6 +152,12 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
 #define LA2_TUNE_PARTITION_BWD 6
 #define LA2_TUNE_PDL 7
 LA2_API int la2_set_tuning(int key, int value);
+
+/* Bytes of the per-(device, stream) workspace on the current device (0 without a
+ * device). Constant in B, H, N: the working set of a pass is independent of the
+ * sequence length (the reference's constant-scratch property, scratch.py /
+ * test_acceptance.py criterion 6). */
+LA2_API long long la2_workspace_bytes(void);
 
 /*
  * Self-test of the tensor-core operand layouts (not a reference replacement):

@@ -28,6 +28,7 @@ from .ops import (
     split_factor,
     split_forward,
     state_scan,
+    workspace_bytes,
 )
 from .sp import exclusive_scan, sp_lightning_attn2
 
@@ -49,4 +50,5 @@ __all__ = [
     "split_factor",
     "split_forward",
     "state_scan",
+    "workspace_bytes",
 ]

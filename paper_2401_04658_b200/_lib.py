@@ -35,11 +35,12 @@ SIGNATURES: dict[str, list] = {
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_set_tuning": [_i, _i],
+    "la2_workspace_bytes": [],
     "la2_selftest_umma": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_bench_umma": [_i, _i, _i, _i, _i, _i, _vp, _vp],
     "la2_bench_tmem": [_i, _i, _i, _i, _vp, _vp, _vp],
 }
-_RESTYPES = {"la2_last_error": ctypes.c_char_p}
+_RESTYPES = {"la2_last_error": ctypes.c_char_p, "la2_workspace_bytes": ctypes.c_longlong}
 _DEV_ONLY = {"la2_set_tuning", "la2_selftest_umma", "la2_bench_umma", "la2_bench_tmem"}
 
 _lib = None

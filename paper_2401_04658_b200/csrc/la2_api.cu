@@ -25,6 +25,10 @@ int set_cuda_error(const char* where, cudaError_t e) {
 // Handoff workspace of the persistent schedule, one per (device, stream) so that
 // kernels on different streams never share flags. Allocated once, zeroed, never freed;
 // the flags return to zero at the end of every launch (each is consumed by its reader).
+static size_t workspace_state_bytes(int slots) {  // d x 64 fp32 state per slot, d <= 128
+  return static_cast<size_t>(slots) * 128 * 64 * sizeof(float);
+}
+
 Workspace get_workspace(cudaStream_t st) {
   struct Entry {
     int dev;
@@ -46,7 +50,7 @@ Workspace get_workspace(cudaStream_t st) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int slots = sms;  // at most one CTA per SM
-  const size_t state_bytes = static_cast<size_t>(slots) * 128 * 64 * sizeof(float);
+  const size_t state_bytes = workspace_state_bytes(slots);
   void* buf = nullptr;
   if (cudaMalloc(&buf, state_bytes + slots * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
@@ -163,6 +167,16 @@ const char* la2_last_error(void) { return g_err; }
 int la2_set_tuning(int key, int value) {
   g_err[0] = 0;
   return set_tuning(key, value);
+}
+
+long long la2_workspace_bytes(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return static_cast<long long>(la2::workspace_state_bytes(sms) + sms * sizeof(int));
 }
 
 int la2_forward(const void* q, const void* k, const void* v, const float* decay, void* o,

@@ -8,8 +8,10 @@ reference applies to its own CPU kernel:
 * ``classify`` and its bands          -- bench.py:35-36, :99-108
 * ``time_pass``                        -- bench.py:165-192 (median of >= 3 reps after a
                                           warm-up; device time from CUDA events; the
-                                          scratch column is the device memory the pass
-                                          allocates beyond its inputs)
+                                          scratch column follows scratch.py: working
+                                          memory the pass allocates beyond its inputs
+                                          and returned outputs, plus the library's fixed
+                                          workspace)
 * ``scaling_sweep`` / ``_check_n_list`` -- bench.py:230-261 (strictly doubling n, >= 4
                                           points; "tiled" is timed fwd+bwd, "chunked" /
                                           "recurrent" forward only, as SWEEP_DIRECTIONS)
@@ -135,16 +137,26 @@ def _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads=1, bat
     def backward():
         ops.la2_backward(q, k, v, do, dec)
 
+    e = torch.tensor([], dtype=dtype).element_size()
+    o_b, g_b = batch * heads * n * dv * e, batch * heads * n * (2 * d + dv) * e
+    st_b = batch * heads * d * dv * 4
+    if impl == "tiled":
+        outputs = {"forward": o_b, "backward": g_b, "fwd+bwd": max(o_b, g_b)}[direction]
+    elif impl == "chunked":  # one chunk's o plus the carried state, old and new
+        outputs = batch * heads * -(-n // STREAM_CHUNKS) * dv * e + 2 * st_b
+    else:  # the state and one step's o (old and new)
+        outputs = st_b + 2 * batch * heads * dv * e
+
     if direction == "forward":
-        return forward
+        return forward, outputs
     if direction == "backward":
-        return backward
+        return backward, outputs
 
     def both():
         forward()
         backward()
 
-    return both
+    return both, outputs
 
 
 def time_pass(impl: str, direction: str, n: int, d: int = 64, dv: int = None, block: int = 64,
@@ -158,13 +170,13 @@ def time_pass(impl: str, direction: str, n: int, d: int = 64, dv: int = None, bl
     dv = d if dv is None else dv
     device = device or torch.device("cuda", torch.cuda.current_device())
     try:
-        run = _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads, batch)
+        run, outputs = _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads, batch)
         torch.cuda.synchronize(device)
         base = torch.cuda.memory_allocated(device)
         torch.cuda.reset_peak_memory_stats(device)
         run()
         torch.cuda.synchronize(device)
-        scratch = max(0, torch.cuda.max_memory_allocated(device) - base)
+        scratch = max(0, torch.cuda.max_memory_allocated(device) - base - outputs) + ops.workspace_bytes()
         times = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -224,13 +236,15 @@ ACCEPTANCE_SPREAD = 1.5
 
 
 def acceptance_scaling(heads: int = 128, dtype=torch.bfloat16, reps: int = 5):
-    """Criterion 5 of the reference (test_acceptance.py:129-144) on the GPU path:
-    returns (records, verdict, spread, ok)."""
+    """Criteria 5 and 6 of the reference (test_acceptance.py:129-156) on the GPU path:
+    the tiled sweep is linear-like with per-token spread <= 1.5, and its scratch is the
+    same number of bytes at every n. Returns (records, verdict, spread, ok)."""
     records, verdicts = scaling_sweep(["tiled"], ACCEPTANCE_N, 64, lam=0.9, reps=reps,
                                       dtype=dtype, heads=heads)
     per_tok = [r.per_token_microseconds for r in records]
     spread = max(per_tok) / min(per_tok)
-    ok = verdicts[0].classification == "linear-like" and spread <= ACCEPTANCE_SPREAD
+    ok = (verdicts[0].classification == "linear-like" and spread <= ACCEPTANCE_SPREAD
+          and len({r.scratch_bytes for r in records}) == 1)
     return records, verdicts[0], spread, ok
 
 
@@ -274,7 +288,9 @@ def main(argv=None) -> int:
             per_tok = [r.per_token_microseconds for r in records if r.impl == "tiled"]
             spread = max(per_tok) / min(per_tok)
             print(f"tiled per-token max/min {spread:.2f} (criterion 5 needs <= {ACCEPTANCE_SPREAD})")
-            ok = ok and spread <= ACCEPTANCE_SPREAD
+            scratch = sorted({r.scratch_bytes for r in records if r.impl == "tiled"})
+            print(f"tiled scratch bytes per n: {scratch} (criterion 6 needs one value)")
+            ok = ok and spread <= ACCEPTANCE_SPREAD and len(scratch) == 1
     return 0 if ok else 1
 
 

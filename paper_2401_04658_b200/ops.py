@@ -261,6 +261,12 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
 TUNE_PERSISTENT, TUNE_PREFETCH, TUNE_L2HINT, TUNE_FUSED_BWD, TUNE_CONCURRENT_BWD, TUNE_PARTITION_BWD, TUNE_PDL = 1, 2, 3, 4, 5, 6, 7
 
 
+def workspace_bytes() -> int:
+    """Bytes of the library's fixed per-(device, stream) workspace on the current device
+    (include/la2.h la2_workspace_bytes); independent of B, H and N."""
+    return int(_lib.load().la2_workspace_bytes())
+
+
 def set_tuning(key: int, value: int) -> None:
     """Process-wide scheduling knob of the tensor-core kernels (include/la2.h
     la2_set_tuning). Outputs do not depend on it."""

@@ -584,12 +584,15 @@ def test_gpubench_sweep_and_block_invariance():
 
 
 def test_acceptance_criterion_5_on_gpu():
-    """The reference's scaling acceptance (test_acceptance.py:51-62, :129-144): tiled
-    fwd+bwd over n = 8K..64K at d = 64 is linear-like with per-token spread <= 1.5 --
-    here on the GPU path (bf16, 128 heads so one call fills the B200)."""
+    """The reference's scaling acceptance (test_acceptance.py:51-62, :129-156): tiled
+    fwd+bwd over n = 8K..64K at d = 64 is linear-like with per-token spread <= 1.5 and
+    a constant working set -- here on the GPU path (bf16, 128 heads: one call fills
+    the B200)."""
     from paper_2401_04658_b200 import gpubench as gb
     recs, verdict, spread, ok = gb.acceptance_scaling(heads=128, reps=5)
     assert [r.n for r in recs] == list(gb.ACCEPTANCE_N)
+    # criterion 6: constant working set -- the library's fixed workspace at every n
+    assert {r.scratch_bytes for r in recs} == {la2.ops.workspace_bytes()}
     assert ok, (verdict.ratios, verdict.classification, spread)
 
 
