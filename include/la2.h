@@ -69,6 +69,19 @@ LA2_API int la2_forward(const void* q, const void* k, const void* v, const float
                 void* stream);
 
 /*
+ * la2_forward on views: q, k, v may have any element stride between consecutive (b, h)
+ * rows (ldq, ldk, ldv >= N * d / N * dv, multiples of 8), e.g. a [B, H, N, d] slice of
+ * a longer sequence, so streaming over chunks of a resident sequence reads the chunks in
+ * place (chunked_forward on slices, kernel.py:142-162). o, kv_in, kv_out contiguous.
+ * Tensor-core shapes only (bf16, d in {64,128}, dv % 64 == 0); otherwise
+ * LA2_ERR_UNSUPPORTED.
+ */
+LA2_API int la2_forward_strided(const void* q, const void* k, const void* v, const float* decay,
+                                void* o, const float* kv_in, float* kv_out, int B, int H, int N,
+                                int d, int dv, int dtype, long long ldq, long long ldk,
+                                long long ldv, void* stream);
+
+/*
  * Backward pass: gradients of sum(dout * O) with respect to q, k, v.
  * Replaces tila.tiled_backward     (pkg/src/tila/kernel.py:165-233) and
  *          tila.batched_backward   (pkg/src/tila/kernel.py:263-266).

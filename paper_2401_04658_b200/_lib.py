@@ -29,6 +29,8 @@ SIGNATURES: dict[str, list] = {
     "la2_version": [],
     "la2_last_error": [],
     "la2_forward": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_forward_strided": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
+                            ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _vp],
     "la2_backward": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_chunk_state": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],

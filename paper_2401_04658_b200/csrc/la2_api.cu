@@ -190,6 +190,29 @@ int la2_forward(const void* q, const void* k, const void* v, const float* decay,
   return run_f(a, static_cast<cudaStream_t>(stream));
 }
 
+int la2_forward_strided(const void* q, const void* k, const void* v, const float* decay, void* o,
+                        const float* kv_in, float* kv_out, int B, int H, int N, int d, int dv,
+                        int dtype, long long ldq, long long ldk, long long ldv, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (!q || !k || !v || !o) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (!tc_eligible(dtype, d, dv))
+    return set_error(LA2_ERR_UNSUPPORTED,
+                     "strided inputs need the tensor-core path (bf16, d in {64,128}, dv % 64 == 0)");
+  const long long need[3] = {1LL * N * d, 1LL * N * d, 1LL * N * dv};
+  const long long ld[3] = {ldq, ldk, ldv};
+  for (int t = 0; t < 3; ++t)
+    if (ld[t] < need[t] || (ld[t] * 2) % 16 != 0)
+      return set_error(LA2_ERR_VALUE,
+                       "head stride must be >= N * cols elements and a multiple of 8 (16 bytes)");
+  if (int rc = bind_device(stream, q)) return rc;
+  FArgs a{q, k, v, o, decay, kv_in, 0, kv_out, B, H, N, d, dv, dtype, 0};
+  a.ld[0] = ldq;
+  a.ld[1] = ldk;
+  a.ld[2] = ldv;
+  return run_f(a, static_cast<cudaStream_t>(stream));
+}
+
 static int backward_reverse(const void* q, const void* k, const void* v, const void* dout,
                             const float* decay, void* dk, void* dv, const float* dkv_in,
                             float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,

@@ -23,6 +23,9 @@ struct FArgs {
   int dtype;
   int reverse;
   int max_ranges = 0;  // persistent schedule: cap on co-resident work ranges (0 = all SMs)
+  // elements between consecutive (b, h) rows of q, k, v, o (0 = contiguous N * cols);
+  // tensor-core path only (the TMA maps carry the stride)
+  long long ld[4] = {0, 0, 0, 0};
 };
 
 // Kernel-side parameter block (passed by value).
@@ -51,9 +54,10 @@ int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 int launch_g(const void* q, const void* k, const void* v, const void* dout, void* dk, void* dv,
              const float* decay, const float* dkv_in, float* dkv_out, int B, int H, int N,
              cudaStream_t st);
-// TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle.
+// TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle;
+// head_stride = elements between (b, h) rows (0: N * cols).
 int tma_encoder_ready();
-int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows);
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows, long long head_stride = 0);
 int launch_simt(const FArgs& a, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);

@@ -868,37 +868,43 @@ static int get_encode() {
 }
 
 // [BH][N][cols] bf16, box (64 cols, 128 rows, 1 head), 128B swizzle.
-int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows);
+// (make_tmap_bf16 is declared in la2_kernels.h)
 int tma_encoder_ready() { return get_encode(); }
 // Tensor maps depend only on (address, shape, box), so they are cached per host thread
 // (a map for the same address and shape is valid whatever tensor now lives there).
-static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT) {
+static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT,
+                     long long head_stride = 0) {
   struct Entry {
     const void* ptr;
     int cols, N, BH, box;
+    long long ld;
     CUtensorMap map;
   };
   static thread_local Entry cache[32];
   static thread_local int next = 0;
   for (const Entry& e : cache) {
-    if (e.ptr == ptr && e.cols == cols && e.N == N && e.BH == BH && e.box == box_rows && ptr) {
+    if (e.ptr == ptr && e.cols == cols && e.N == N && e.BH == BH && e.box == box_rows &&
+        e.ld == head_stride && ptr) {
       *m = e.map;
       return 0;
     }
   }
-  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows);
+  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows, head_stride);
   if (rc == 0) {
     Entry& e = cache[next];
     next = (next + 1) & 31;
-    e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.map = *m;
+    e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.ld = head_stride;
+    e.map = *m;
   }
   return rc;
 }
-int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows) {
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows,
+                   long long head_stride) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
                         static_cast<cuuint64_t>(BH)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2,
-                           static_cast<cuuint64_t>(cols) * 2 * static_cast<cuuint64_t>(N)};
+  const cuuint64_t ld = head_stride > 0 ? static_cast<cuuint64_t>(head_stride)
+                                        : static_cast<cuuint64_t>(cols) * static_cast<cuuint64_t>(N);
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, ld * 2};
   cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
@@ -975,7 +981,8 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   for (int t = 0; t < 8; ++t) {
     if (SO && t != 1 && t != 2) continue;
     if (CM != 3 && (t == 5 || t == 6)) continue;
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT);
+    const long long ld = (t < 4) ? a.ld[t] : (a1 ? a1->ld[t - 4] : a.ld[t - 4]);
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT, ld);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),

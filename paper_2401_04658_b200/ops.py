@@ -225,14 +225,44 @@ def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
     (pkg/src/tila/kernel.py:142-162); kv_out its returned KvState.kv.
     """
     B, H, N, d, dv = _check_qkv(q, k, v)
-    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
-    o = torch.empty_like(v)
     kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
+    lds = None
+    if q.dtype == torch.bfloat16 and d in (64, 128) and dv % 64 == 0 and not (
+            q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+        lds = [_head_stride(t) for t in (q, k, v)]
+        if any(x is None for x in lds):
+            lds = None
+    if lds is not None:  # views (e.g. a chunk of a resident sequence): read in place
+        o = torch.empty(B, H, N, dv, device=v.device, dtype=v.dtype)
+        _lib.call("la2_forward_strided", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in),
+                  _ptr(kv_out), B, H, N, d, dv, _code(q), lds[0], lds[1], lds[2], _stream(q.device))
+        return o, kv_out
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(v)
     _lib.call("la2_forward", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in), _ptr(kv_out),
               B, H, N, d, dv, _code(q), _stream(q.device))
     return o, kv_out
+
+
+def _head_stride(t: torch.Tensor) -> Optional[int]:
+    """Element stride between consecutive (b, h) rows of a [B,H,N,c] view whose rows are
+    contiguous and evenly spaced (la2_forward_strided), else None."""
+    B, H, N, c = t.shape
+    if t.stride(3) != 1 or (N > 1 and t.stride(2) != c) or t.data_ptr() % 16:
+        return None
+    if B > 1 and H > 1:
+        ld = t.stride(1) if t.stride(0) == H * t.stride(1) else None
+    elif H > 1:
+        ld = t.stride(1)
+    elif B > 1:
+        ld = t.stride(0)
+    else:
+        ld = N * c
+    if ld is None or ld < N * c or ld % 8:
+        return None
+    return ld
 
 
 def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, output_dkv: bool = False):

@@ -683,3 +683,29 @@ def test_host_decay_upload_cached():
     for bad in ([0.9, 1.5, 1.0], [0.0, 0.5, 0.5], [0.5, 0.5]):
         with pytest.raises(ValueError):
             ops._decay(bad, 3, DEV)
+
+
+@pytest.mark.parametrize("B,H,d,dv", [(2, 3, 64, 64), (1, 4, 128, 128), (2, 1, 64, 128), (3, 2, 128, 64)])
+def test_forward_on_views_reads_in_place(B, H, d, dv):
+    """la2_forward on [B,H,N,d] slices of a longer resident sequence (la2_forward_strided:
+    TMA maps with the view's head stride, no copies) equals the contiguous call bitwise,
+    and streaming the chunks with the carried state equals the one-shot forward."""
+    from paper_2401_04658_b200 import ops
+    N = 1000
+    q, k, v, _ = inputs(B, H, N, d, dv, torch.bfloat16, seed=88)
+    qg, kg, vg = gpu(q, k, v)
+    decay = [0.95, 0.999, 1.0, 0.9][:H]
+    ref_o, ref_kv = la2.la2_forward(qg, kg, vg, decay, output_final_state=True)
+    st, outs = None, []
+    for a, b in [(0, 128), (128, 384), (384, 391), (391, 1000)]:
+        qs, ks, vs = qg[:, :, a:b], kg[:, :, a:b], vg[:, :, a:b]
+        assert not qs.is_contiguous() and ops._head_stride(qs) == N * d
+        o, st2 = la2.la2_forward(qs, ks, vs, decay, kv_in=st, output_final_state=True)
+        oc, stc = la2.la2_forward(qs.contiguous(), ks.contiguous(), vs.contiguous(), decay, kv_in=st,
+                                  output_final_state=True)
+        assert torch.equal(o, oc) and torch.equal(st2, stc)
+        outs.append(o)
+        st = st2
+    # ragged chunk boundaries round the bf16 fold operands differently: bf16 tolerance
+    assert rel(torch.cat(outs, 2), to64(ref_o)) <= BF16_TOL
+    assert rel(st, to64(ref_kv)) <= BF16_TOL
