@@ -185,6 +185,52 @@ def cpu_reference(n: int, d: int, heads_total: int, tokens_per_step: int, sample
 
 
 # ------------------------------------------------------------------ GPU side
+def c5_phases(q, k, v, do, dec, world, timed_phase):
+    """C5 per-rank time split: pass A (chunk states), the exchange (state
+    scan across ranks -- NCCL -- or across the intra-GPU chunks), pass B (the F passes
+    with the carried states), forward and backward, each timed alone on the device."""
+    from paper_2401_04658_b200 import ops
+    from paper_2401_04658_b200.sp import exclusive_scan
+    B, H, L, D = q.shape
+    res = {}
+    if world > 1:
+        mode = os.environ.get("LA2_SP_MODE", "allgather")
+        s = ops.chunk_state(k, v, dec)
+        kv_in = exclusive_scan(s, dec, L, None, reverse=False, mode=mode)
+        t = ops.chunk_dstate(q, do, dec)
+        dkv_in = exclusive_scan(t, dec, L, None, reverse=True, mode=mode)
+        res["fwd_pass_a"] = timed_phase(lambda: ops.chunk_state(k, v, dec))
+        res["fwd_exchange"] = timed_phase(lambda: exclusive_scan(s, dec, L, None, mode=mode))
+        res["fwd_pass_b"] = timed_phase(lambda: ops.la2_forward(q, k, v, dec, kv_in=kv_in))
+        res["bwd_pass_a"] = timed_phase(lambda: ops.chunk_dstate(q, do, dec))
+        res["bwd_exchange"] = timed_phase(lambda: exclusive_scan(t, dec, L, None, reverse=True, mode=mode))
+        res["bwd_pass_b"] = timed_phase(lambda: ops.la2_backward(q, k, v, do, dec, kv_in=kv_in,
+                                                                 dkv_in=dkv_in))
+        res["exchange_bytes_per_direction"] = 2 * world * H * D * D * 4
+        return res
+    g = ops.split_factor(B, H, L, D, D, q.dtype)
+    if g == 1:
+        return {"note": "no split at this shape"}
+    dec_g = dec.repeat_interleave(g)
+    q4, k4, v4, do4 = (ops._chunked(x.contiguous(), g) for x in (q, k, v, do))
+    lens = [L // g] * g
+    s = ops.chunk_state(k4, v4, dec_g)
+    s5 = ops._to_chunk_major(s, B, H, g)
+    prefix = ops._from_chunk_major(ops.state_scan(s5, dec, lens), B, H, g)
+    t = ops.chunk_dstate(q4, do4, dec_g)
+    t5 = ops._to_chunk_major(t, B, H, g)
+    suffix = ops._from_chunk_major(ops.state_scan(t5, dec, lens, reverse=True), B, H, g)
+    res["chunks"] = g
+    res["fwd_pass_a"] = timed_phase(lambda: ops.chunk_state(k4, v4, dec_g))
+    res["fwd_exchange"] = timed_phase(lambda: ops.state_scan(s5, dec, lens))
+    res["fwd_pass_b"] = timed_phase(lambda: ops.la2_forward(q4, k4, v4, dec_g, kv_in=prefix))
+    res["bwd_pass_a"] = timed_phase(lambda: ops.chunk_dstate(q4, do4, dec_g))
+    res["bwd_exchange"] = timed_phase(lambda: ops.state_scan(t5, dec, lens, reverse=True))
+    res["bwd_pass_b"] = timed_phase(lambda: ops.la2_backward(q4, k4, v4, do4, dec_g, kv_in=prefix,
+                                                             dkv_in=suffix))
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -400,6 +446,18 @@ def extra_workload(args, world, rank, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def timed_phase(fn, reps=5):
+        """Device time of one phase (CUDA events, max over ranks); fn returns nothing."""
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / reps)
+
     def timed(fn, steps, warmup=3):
         for _ in range(warmup):
             fn()
@@ -516,12 +574,14 @@ def extra_workload(args, world, rank, local_rank):
                 o.backward(do)
             mode = f"sequence parallel x{world} ({os.environ.get('LA2_SP_MODE', 'allgather')}) "
         ms = timed(step, args.steps)
+        phases = c5_phases(q.detach(), k.detach(), v.detach(), do, dec, world, timed_phase)
         ff, fb = canonical_flops(N_total, D, D)
         bf, bb = canonical_bytes(N_total, D, D)
         line.update({"metric": "c5 fwd+bwd tokens/s (one 512K sequence)", "value": N_total / (ms / 1e3),
                      "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "dtype": "bf16",
                      "config": {"workload": "c5", "seq_len": N_total, "heads": H, "head_dim": D,
                                 "per_rank_tokens": L, "mode": mode},
+                     "phases_ms": phases,
                      "tflops": (ff + fb) * H / (ms / 1e3) / 1e12,
                      "frac_of_roof": max((ff + fb) * H / (tc_peak * 1e12 * world),
                                          (bf + bb) * H / (hbm_peak * 1e9 * world)) * 1e3 / ms})

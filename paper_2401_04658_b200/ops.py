@@ -146,8 +146,8 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     Q,dO in the backward). Tensor-core path: used when units < ~100, chunks stay
     >= 8192 tokens and the split is at least 4-way (measured: at B=1, H=8, N=8192 the
     unsplit fwd+bwd takes 0.20 ms and every split 0.33-0.37 ms; at H=16, N=16384 splits
-    are within noise of no split; at H=4, N=64K an 8-way split is 4.7x faster). SIMT path (fp32 / other shapes, several CTAs per SM): split until
-    ~4 units per SM, down to 32-token chunks at d <= 64 (128 above), at most 64 chunks
+    are within noise of no split; at H=4, N=64K an 8-way split is 4.7x faster).
+    SIMT path (fp32 / other shapes, several CTAs per SM): split until ~4 units per SM, down to 32-token chunks at d <= 64 (128 above), at most 64 chunks
     (the state scan's limit). Measured on B200 (tools/fp32_split.py): C1 fp32 fwd+bwd
     1.22 ms at 8 chunks -> 0.53 ms at 64.
     """
