@@ -54,9 +54,14 @@ constexpr int WC = WY + 1;      // V~ copy warp
 // barrier (fewer spinning warps: less issue pressure and power, one more bar.sync).
 constexpr bool GW = (LA2_GROUP_WAIT != 0);
 
+#ifndef LA2_SO_NS
+#define LA2_SO_NS 4
+#endif
+
 template <int DK, bool SO>
 struct TcLayout {
-  static constexpr int NS = (DK == 64) ? 3 : 2;   // Q/K/V stages
+  // Q/K/V stages; state-only passes stage only K and V (32 / 48 KB), so they get a deeper ring
+  static constexpr int NS = SO ? LA2_SO_NS : ((DK == 64) ? 3 : 2);
   static constexpr int KTS = 2;                   // V~ buffers (scaled values)
   static constexpr int OS = (DK == 64 && !SO) ? 2 : 1;  // O staging buffers
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
