@@ -126,3 +126,16 @@ def test_cli_usage_errors_exit_2():
         assert e.value.code == 2
     args = cli.build_parser().parse_args(["stream-demo", "--dim", "64", "--chunk", "100", "--chunks", "3"])
     assert args.lam == cli.BENCH_LAMBDA
+
+
+def test_bench_roofline_traffic_source():
+    """bench.py's roofline.traffic comes from the committed ncu summary: the file keeps
+    the per-token-head DRAM bytes of the forward F launch, close to the algorithmic 512."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import bench
+    per = bench.load_traffic(1)
+    assert per is not None and 0.9 * 512 <= per <= 1.1 * 512, per
+    assert bench.load_traffic(8 * 16 * 65536) == per * 8 * 16 * 65536
