@@ -709,3 +709,24 @@ def test_forward_on_views_reads_in_place(B, H, d, dv):
     # ragged chunk boundaries round the bf16 fold operands differently: bf16 tolerance
     assert rel(torch.cat(outs, 2), to64(ref_o)) <= BF16_TOL
     assert rel(st, to64(ref_kv)) <= BF16_TOL
+
+
+def test_forward_strided_abi_errors():
+    """la2_forward_strided rejects head strides below N*cols or not 16-byte multiples
+    (LA2_ERR_VALUE) and non-tensor-core shapes (LA2_ERR_UNSUPPORTED), without launching."""
+    from paper_2401_04658_b200 import _lib, ops
+    lib = _lib.load()
+    B, H, N, d = 1, 2, 256, 64
+    q, k, v, _ = gpu(*inputs(B, H, N, d, d, torch.bfloat16, seed=5))
+    dec = ops._decay([0.9, 0.9], H, DEV)
+    o = torch.empty_like(v)
+    st = ops._stream(q.device)
+    call = lambda ld, dt=0, dd=d: lib.la2_forward_strided(
+        ops._ptr(q), ops._ptr(k), ops._ptr(v), ops._ptr(dec), ops._ptr(o), None, None,
+        B, H, N, dd, dd, dt, ld, ld, ld, st)
+    assert call(N * d) == 0
+    assert call(N * d - 8) == _lib.LA2_ERR_VALUE
+    assert call(N * d + 4) == _lib.LA2_ERR_VALUE
+    assert call(N * d, dt=1) == _lib.LA2_ERR_UNSUPPORTED
+    assert call(N * 32, dd=32) == _lib.LA2_ERR_UNSUPPORTED
+    torch.cuda.synchronize()
