@@ -96,6 +96,18 @@ LA2_API int la2_backward(const void* q, const void* k, const void* v, const void
                  int dtype, void* stream);
 
 /*
+ * la2_backward on views: q, k, v, dout with (b, h) row strides ldq, ldk, ldv, lddo
+ * (>= N * d / N * dv elements, multiples of 8), e.g. chunks of a resident sequence
+ * (training on sequence chunks with the carried kv_in / dkv_in); dq, dk, dv contiguous.
+ * Tensor-core shapes only; otherwise LA2_ERR_UNSUPPORTED.
+ */
+LA2_API int la2_backward_strided(const void* q, const void* k, const void* v, const void* dout,
+                                 const float* decay, void* dq, void* dk, void* dv,
+                                 const float* kv_in, const float* dkv_in, float* dkv_out, int B,
+                                 int H, int N, int d, int dvd, int dtype, long long ldq,
+                                 long long ldk, long long ldv, long long lddo, void* stream);
+
+/*
  * Chunk-local forward state only (no output): S = sum_s lam^(N-1-s) k_s^T v_s.
  * Equals the KvState.kv returned by tila.chunked_forward from a fresh state
  * (pkg/src/tila/kernel.py:142-162). Sequence-parallel pass A.

@@ -32,6 +32,8 @@ SIGNATURES: dict[str, list] = {
     "la2_forward_strided": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
                             ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _vp],
     "la2_backward": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_backward_strided": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
+                             ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, _vp],
     "la2_chunk_state": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],

@@ -216,11 +216,52 @@ int la2_forward_strided(const void* q, const void* k, const void* v, const float
 static int backward_reverse(const void* q, const void* k, const void* v, const void* dout,
                             const float* decay, void* dk, void* dv, const float* dkv_in,
                             float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,
-                            cudaStream_t st, int max_ranges = 0);
+                            cudaStream_t st, int max_ranges = 0, const long long* ld = nullptr);
+
+// (b, h) row strides of the operands of one F pass, by role, from the caller's
+// q / k / v / dout strides (nullptr: all contiguous)
+static void set_ld(FArgs& a, const long long* ld, int iq, int ik, int iv) {
+  if (ld == nullptr) return;
+  a.ld[0] = ld[iq];
+  a.ld[1] = ld[ik];
+  a.ld[2] = ld[iv];
+}
+
+static int backward_impl(const void* q, const void* k, const void* v, const void* dout,
+                         const float* decay, void* dq, void* dk, void* dv, const float* kv_in,
+                         const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dvd,
+                         int dtype, void* stream, const long long* ld);
 
 int la2_backward(const void* q, const void* k, const void* v, const void* dout, const float* decay,
                  void* dq, void* dk, void* dv, const float* kv_in, const float* dkv_in,
                  float* dkv_out, int B, int H, int N, int d, int dvd, int dtype, void* stream) {
+  return backward_impl(q, k, v, dout, decay, dq, dk, dv, kv_in, dkv_in, dkv_out, B, H, N, d, dvd,
+                       dtype, stream, nullptr);
+}
+
+int la2_backward_strided(const void* q, const void* k, const void* v, const void* dout,
+                         const float* decay, void* dq, void* dk, void* dv, const float* kv_in,
+                         const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dvd,
+                         int dtype, long long ldq, long long ldk, long long ldv, long long lddo,
+                         void* stream) {
+  g_err[0] = 0;
+  if (!tc_eligible(dtype, d, dvd))
+    return set_error(LA2_ERR_UNSUPPORTED,
+                     "strided inputs need the tensor-core path (bf16, d in {64,128}, dv % 64 == 0)");
+  const long long ld[4] = {ldq, ldk, ldv, lddo};
+  const long long need[4] = {1LL * N * d, 1LL * N * d, 1LL * N * dvd, 1LL * N * dvd};
+  for (int t = 0; t < 4; ++t)
+    if (ld[t] < need[t] || (ld[t] * 2) % 16 != 0)
+      return set_error(LA2_ERR_VALUE,
+                       "head stride must be >= N * cols elements and a multiple of 8 (16 bytes)");
+  return backward_impl(q, k, v, dout, decay, dq, dk, dv, kv_in, dkv_in, dkv_out, B, H, N, d, dvd,
+                       dtype, stream, ld);
+}
+
+static int backward_impl(const void* q, const void* k, const void* v, const void* dout,
+                         const float* decay, void* dq, void* dk, void* dv, const float* kv_in,
+                         const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dvd,
+                         int dtype, void* stream, const long long* ld) {
   g_err[0] = 0;
   if (int rc = check_common(B, H, N, d, dvd, dtype, decay)) return rc;
   if (int rc = check_common(B, H, N, dvd, d, dtype, decay)) return rc;
@@ -232,6 +273,7 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
   // It shares no output with the dK/dV scans, so for short sequences (where each launch
   // is dominated by its fill / drain) it runs on a forked side stream concurrently.
   FArgs aq{dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, dtype, 0};
+  set_ld(aq, ld, 3, 2, 1);  // dO, V, K
   // d = 64 with enough heads: the dQ scan (128 of 148 SMs at B*H = 128) and the dK/dV pair
   // are both bound by the per-SM block rate and dominated by fill/drain for short
   // sequences, so they run concurrently on disjoint SM partitions sized to the work
@@ -248,7 +290,7 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
     if (ps != nullptr && cudaEventRecord(ps->fork, st) == cudaSuccess &&
         cudaStreamWaitEvent(ps->s, ps->fork, 0) == cudaSuccess) {
       const int rc = backward_reverse(q, k, v, dout, decay, dk, dv, dkv_in, dkv_out, B, H, N, d,
-                                      dvd, dtype, st, pair_cap);
+                                      dvd, dtype, st, pair_cap, ld);
       aq.max_ranges = dq_cap;
       const int rq = rc ? 0 : run_f(aq, ps->s);
       const int jr = join_side(ps, st);
@@ -268,7 +310,8 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
     if (side) join_side(side, st);
     return rc;
   }
-  const int rc = backward_reverse(q, k, v, dout, decay, dk, dv, dkv_in, dkv_out, B, H, N, d, dvd, dtype, st);
+  const int rc = backward_reverse(q, k, v, dout, decay, dk, dv, dkv_in, dkv_out, B, H, N, d, dvd, dtype, st,
+                                  0, ld);
   if (side) {
     if (int jr = join_side(side, st)) return rc ? rc : jr;
   }
@@ -279,29 +322,35 @@ int la2_backward(const void* q, const void* k, const void* v, const void* dout, 
 static int backward_reverse(const void* q, const void* k, const void* v, const void* dout,
                             const float* decay, void* dk, void* dv, const float* dkv_in,
                             float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,
-                            cudaStream_t st, int max_ranges) {
+                            cudaStream_t st, int max_ranges, const long long* ld) {
   // d = dv = 64 bf16: dK and dV in one fused reverse scan (sweep 2, kernel.py:207-231)
   // (experimental single-kernel dK/dV scan, la2_bwd.cu; opt-in: slower than the pair below)
   static const bool fused_g = std::getenv("LA2_FUSED_BWD_G") != nullptr;
-  if (fused_g && dtype == LA2_BF16 && d == 64 && dvd == 64)
+  if (fused_g && ld == nullptr && dtype == LA2_BF16 && d == 64 && dvd == 64)
     return launch_g(q, k, v, dout, dk, dv, decay, dkv_in, dkv_out, B, H, N, st);
   if (dtype == LA2_BF16 && d == 64 && dvd == 64) {
     // dV and dK scans as one cluster pair sharing the Q and dO tiles (sweep 2, kernel.py:207-231)
     FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1, max_ranges};
     FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1, max_ranges};
+    set_ld(av, ld, 1, 0, 3);  // K, Q, dO
+    set_ld(ak, ld, 2, 3, 0);  // V, dO, Q
     return launch_tc_pair(av, ak, st);
   }
   if (dtype == LA2_BF16 && d == 128 && dvd == 128) {
     // dV and dK scans as one 4-CTA cluster per unit (sweep 2, kernel.py:207-231)
     FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
     FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+    set_ld(av, ld, 1, 0, 3);
+    set_ld(ak, ld, 2, 3, 0);
     return launch_tc_quad(av, ak, st);
   }
   // dK = F_rev(V, dO, Q): reverse scan, state dKV^T  (sweep 2, kernel.py:207-216)
   FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+  set_ld(ak, ld, 2, 3, 0);
   if (int rc = run_f(ak, st)) return rc;
   // dV = F_rev(K, Q, dO): reverse scan, state dKV   (sweep 2, kernel.py:217-231)
   FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
+  set_ld(av, ld, 1, 0, 3);
   return run_f(av, st);
 }
 

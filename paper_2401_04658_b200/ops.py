@@ -276,12 +276,26 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     B, H, N, d, dv = _check_qkv(q, k, v)
     if d_out.shape != v.shape or d_out.dtype != v.dtype:
         raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
-    q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
     dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
-    dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dkv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_dkv else None
+    ts = (q, k, v, d_out)
+    lds = None
+    if q.dtype == torch.bfloat16 and d in (64, 128) and dv % 64 == 0 and not all(t.is_contiguous() for t in ts):
+        lds = [_head_stride(t) for t in ts]
+        if any(x is None for x in lds):
+            lds = None
+    if lds is not None:  # views (chunks of a resident sequence): read in place
+        dq = torch.empty(B, H, N, d, device=q.device, dtype=q.dtype)
+        dk = torch.empty(B, H, N, d, device=q.device, dtype=q.dtype)
+        dvv = torch.empty(B, H, N, dv, device=q.device, dtype=q.dtype)
+        _lib.call("la2_backward_strided", _ptr(q), _ptr(k), _ptr(v), _ptr(d_out), _ptr(dec), _ptr(dq),
+                  _ptr(dk), _ptr(dvv), _ptr(kv_in), _ptr(dkv_in), _ptr(dkv_out), B, H, N, d, dv, _code(q),
+                  lds[0], lds[1], lds[2], lds[3], _stream(q.device))
+        return dq, dk, dvv, dkv_out
+    q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
+    dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     _lib.call("la2_backward", _ptr(q), _ptr(k), _ptr(v), _ptr(d_out), _ptr(dec), _ptr(dq), _ptr(dk),
               _ptr(dvv), _ptr(kv_in), _ptr(dkv_in), _ptr(dkv_out), B, H, N, d, dv, _code(q),
               _stream(q.device))
