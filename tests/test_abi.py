@@ -78,3 +78,25 @@ def test_check_maps_codes_to_python_errors(lib):
 
     with pytest.raises(ValueError):
         _lib.call("la2_forward", 16, 16, 16, 16, 16, None, None, 1, 1, 0, 64, 64, 0, None)
+
+
+def test_header_is_plain_c_and_links(lib, tmp_path):
+    """The boundary is usable from C (what a cgo / JNI / N-API shim compiles against):
+    la2.h compiles as C99 with -Wall -Werror and a C program links against libla2.so and
+    calls an entry point."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "use_la2.c"
+    src.write_text('#include "la2.h"\n#include <stdio.h>\n'
+                   'int main(void) { int v = la2_version(); '
+                   'int rc = la2_forward(0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 64, 64, LA2_BF16, 0); '
+                   'printf("%d %d\\n", v, rc); return (v > 0 && rc == LA2_ERR_VALUE) ? 0 : 1; }\n')
+    libdir = ROOT / "paper_2401_04658_b200"
+    exe = tmp_path / "use_la2"
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(src),
+                    f"-L{libdir}", "-l:libla2.so", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    res = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout + res.stderr
