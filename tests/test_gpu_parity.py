@@ -758,3 +758,22 @@ def test_backward_on_views_reads_in_place(B, H, d, dv, N):
     la2.lightning_attn2(qc, kc, vc, decay, seq_split=1).backward(do[:, :, a:b].contiguous())
     for x, y in ((qs, qc), (ks, kc), (vs, vc)):
         assert torch.equal(x.grad, y.grad)
+
+
+@pytest.mark.parametrize("d,dtype", [(64, torch.bfloat16), (128, torch.bfloat16), (64, torch.float32)])
+def test_block_aligned_chunks_bitwise(d, dtype):
+    """The reference's streaming property (pkg/tests/test_kernel.py:190-221):
+    chunks that end on block boundaries reproduce the one-shot forward bit for bit --
+    the carried fp32 state is the one the kernel keeps on chip."""
+    B, H, N = 2, 3, 1024
+    q, k, v, _ = gpu(*inputs(B, H, N, d, d, dtype, seed=61))
+    decay = [0.9, 0.999, 1.0]
+    ref_o, ref_kv = la2.la2_forward(q, k, v, decay, output_final_state=True)
+    blk = 128 if dtype == torch.bfloat16 else 64
+    st, outs = None, []
+    for a, b in [(0, blk), (blk, 4 * blk), (4 * blk, N)]:
+        o, st = la2.la2_forward(q[:, :, a:b].contiguous(), k[:, :, a:b].contiguous(),
+                                v[:, :, a:b].contiguous(), decay, kv_in=st, output_final_state=True)
+        outs.append(o)
+    assert torch.equal(torch.cat(outs, 2), ref_o)
+    assert torch.equal(st, ref_kv)
