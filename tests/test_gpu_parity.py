@@ -777,3 +777,23 @@ def test_block_aligned_chunks_bitwise(d, dtype):
         outs.append(o)
     assert torch.equal(torch.cat(outs, 2), ref_o)
     assert torch.equal(st, ref_kv)
+
+
+def test_acceptance_criterion_7_lam_one_on_gpu():
+    """Criterion 7 of the reference (test_acceptance.py:159-182): with lam = 1 the tiled
+    forward is causal cumulative-sum attention -- 20 instances (n, d, dv, block as the
+    reference draws them) through the tila API on the GPU, vs a directly coded comparator."""
+    worst = 0.0
+    for i in range(20):
+        n = 3 + 13 * (i % 5) + i
+        d = 1 + (i % 4) * 3
+        dv = d + (i % 3)
+        block = 1 + (i * 7) % 40
+        q = tila_api.random_matrix(n, d, 700 + 3 * i)
+        k = tila_api.random_matrix(n, d, 701 + 3 * i)
+        v = tila_api.random_matrix(n, dv, 702 + 3 * i)
+        states = np.cumsum(np.einsum("td,te->tde", k, v), axis=0)
+        want = np.einsum("td,tde->te", q, states)
+        got = tila_api.tiled_forward(q, k, v, 1.0, block).o
+        worst = max(worst, port.rel_err(got, want))
+    assert worst <= FP32_TOL, worst
