@@ -797,3 +797,27 @@ def test_acceptance_criterion_7_lam_one_on_gpu():
         got = tila_api.tiled_forward(q, k, v, 1.0, block).o
         worst = max(worst, port.rel_err(got, want))
     assert worst <= FP32_TOL, worst
+
+
+def test_acceptance_criterion_4_streaming_on_gpu():
+    """Criterion 4 of the reference (test_acceptance.py:100-127): streaming n = 1000 rows
+    (d = 8, lam = 0.9, block 32) through chunked_forward over >= 5 ragged partitions
+    equals the recurrent reference in outputs and final state -- on the GPU."""
+    n, d, lam, block = 1000, 8, 0.9, 32
+    q, k, v = (tila_api.random_matrix(n, d, s) for s in (400, 401, 402))
+    expected, ref_state = port.recurrent_forward(q, k, v, lam)
+    worst = 0.0
+    parts_list = [port.ragged_partition(n, seed) for seed in range(6)]
+    for parts in parts_list:
+        assert sum(parts) == n
+        state = tila_api.KvState.fresh(d, d)
+        outs, start = [], 0
+        for length in parts:
+            o, state = tila_api.chunked_forward(q[start:start + length], k[start:start + length],
+                                                v[start:start + length], lam, block, state)
+            outs.append(o)
+            start += length
+        worst = max(worst, port.rel_err(np.concatenate(outs), expected),
+                    port.rel_err(state.kv, ref_state.kv))
+        assert state.tokens_absorbed == n
+    assert worst <= FP32_TOL, worst
