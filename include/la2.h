@@ -10,7 +10,9 @@
  * memory is one fixed workspace per (device, stream) -- the stream-K state
  * hand-off slots, la2_workspace_bytes() bytes (~4.7 MB on B200), allocated on the
  * first launch on that stream outside graph capture and kept for the process
- * lifetime; it does not grow with B, H or N.
+ * lifetime; it does not grow with B, H or N. A CUDA graph captured on a stream bakes
+ * in that stream's workspace: replays of graphs captured on the same stream must not
+ * run concurrently with each other (capture concurrent graphs on distinct streams).
  *
  * Layouts (all contiguous, row-major):
  *   q, k, dq, dk          [B, H, N, d]
@@ -21,8 +23,14 @@
  *
  * Kernel selection is a pure function of (dtype, d, dv):
  *   bf16, d in {64,128}, dv % 64 == 0   -> tcgen05/TMA tensor-core kernel
- *   otherwise, d <= 128 and dv <= 128   -> SIMT fp32-accumulate kernel
+ *   otherwise, d <= 256 and dv <= 256   -> SIMT fp32-accumulate kernel
  *   anything else                       -> LA2_ERR_UNSUPPORTED (no fallback)
+ *
+ * Decay: the compute entry points read `decay` on the device, asynchronously, so they
+ * cannot return an error for its values. They never clamp: a lambda outside (0, 1]
+ * (or NaN) makes every output of the affected heads NaN. la2_check_decay() is the
+ * validating entry point (the reference's ValueError, reference.py:42-44); the Python
+ * layer calls it once per decay tensor version before the first launch.
  *
  * Return value: 0 on success, a negative LA2_ERR_* code otherwise; the
  * message of the last failure on the calling thread is la2_last_error().
@@ -135,6 +143,15 @@ LA2_API int la2_state_scan(const float* states, const float* decay, const float*
                    int B, int H, int d, int dv, const int* lens, int reverse, void* stream);
 
 /*
+ * Validate a per-head decay vector: every lambda_h must lie in (0, 1]
+ * (tila._check_decay, pkg/src/tila/reference.py:42-44). `decay` may be device memory
+ * (copied to the host on `stream`, which is synchronized: not usable inside graph
+ * capture -> LA2_ERR_UNSUPPORTED) or host memory. Returns LA2_ERR_VALUE with the
+ * offending value and head otherwise.
+ */
+LA2_API int la2_check_decay(const float* decay, int H, void* stream);
+
+/*
  * One decode step per (b, h), in place on `state`:
  *   state <- lam * state + k_t^T v_t ;  o_t = q_t state
  * Replaces tila.inference_step (pkg/src/tila/reference.py:162-181, _decay_step :135-139).
@@ -183,23 +200,6 @@ LA2_API int la2_set_tuning(int key, int value);
  * sequence length (the reference's constant-scratch property, scratch.py /
  * test_acceptance.py criterion 6). */
 LA2_API long long la2_workspace_bytes(void);
-
-/*
- * Self-test of the tensor-core operand layouts (not a reference replacement):
- * D[M][N] = A[M][K] B[K][N] through the same SW128 descriptors the tcgen05
- * kernel uses; a_mn / b_mn select MN-major staging. fp32 device buffers.
- */
-LA2_API int la2_selftest_umma(const float* A, const float* B, float* D, int M, int N, int K,
-                              int a_mn, int b_mn, void* stream);
-
-/* Micro-benchmark of one tcgen05.mma shape (development tool): clock cycles per CTA
- * for `iters` back-to-back K=16 MMAs; a_mode 0/1/2 = A K-major smem / MN-major smem / TMEM. */
-LA2_API int la2_bench_umma(int M, int N, int a_mode, int b_mn, int iters, int ctas, long long* out,
-                           void* stream);
-
-/* Micro-benchmark of TMEM -> register loads (development tool). */
-LA2_API int la2_bench_tmem(int warps, int iters, int batch, int ctas, long long* out, float* sink,
-                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -38,14 +38,22 @@ SIGNATURES: dict[str, list] = {
     "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "la2_check_decay": [_vp, _i, _vp],
     "la2_set_tuning": [_i, _i],
     "la2_workspace_bytes": [],
+}
+_RESTYPES = {"la2_last_error": ctypes.c_char_p, "la2_workspace_bytes": ctypes.c_longlong,
+             "la2_dev_last_error": ctypes.c_char_p}
+_DEV_ONLY = {"la2_set_tuning"}
+
+# development library (include/la2_dev.h): not the shipping ABI
+DEV_LIB_PATH = _PKG / "libla2_dev.so"
+DEV_SIGNATURES: dict[str, list] = {
+    "la2_dev_last_error": [],
     "la2_selftest_umma": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_bench_umma": [_i, _i, _i, _i, _i, _i, _vp, _vp],
     "la2_bench_tmem": [_i, _i, _i, _i, _vp, _vp, _vp],
 }
-_RESTYPES = {"la2_last_error": ctypes.c_char_p, "la2_workspace_bytes": ctypes.c_longlong}
-_DEV_ONLY = {"la2_set_tuning", "la2_selftest_umma", "la2_bench_umma", "la2_bench_tmem"}
 
 _lib = None
 
@@ -89,3 +97,32 @@ def call(name: str, *args) -> None:
     rc = fn(*args)
     if rc:
         check(rc, name)
+
+
+_dev = None
+
+
+def load_dev() -> ctypes.CDLL:
+    """Load the development library libla2_dev.so (self-test and micro-benchmarks)."""
+    global _dev
+    if _dev is not None:
+        return _dev
+    if not DEV_LIB_PATH.exists():
+        raise ImportError(f"{DEV_LIB_PATH} not found: build it with `python -m paper_2401_04658_b200.build`")
+    lib = ctypes.CDLL(str(DEV_LIB_PATH))
+    for name, args in DEV_SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _dev = lib
+    return lib
+
+
+def call_dev(name: str, *args) -> None:
+    lib = load_dev()
+    rc = getattr(lib, name)(*args)
+    if rc:
+        msg = lib.la2_dev_last_error().decode(errors="replace")
+        if rc in (LA2_ERR_VALUE, LA2_ERR_UNSUPPORTED):
+            raise ValueError(f"{name}: {msg}")
+        raise RuntimeError(f"{name}: {msg} (code {rc})")

@@ -17,7 +17,10 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libla2.so"
-SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_bwd.cu", "la2_simt.cu", "la2_selftest.cu"]
+SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_simt.cu"]
+# development library (include/la2_dev.h): operand-layout self-test and micro-benchmarks
+DEV_LIB = PKG / "libla2_dev.so"
+DEV_SOURCES = ["la2_selftest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -42,24 +45,30 @@ def _compile(src: str, verbose: bool, extra=(), tag="") -> Path:
     return obj
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path, sources) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
-    deps.append(ROOT / "include" / "la2.h")
+    t = lib.stat().st_mtime
+    deps = [CSRC / s for s in sources] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+    deps += list((ROOT / "include").glob("*.h"))
     return any(p.stat().st_mtime > t for p in deps)
 
 
 def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
-    """Build libla2.so (or, with trace=True, the phase-trace variant libla2_trace.so)."""
-    lib = PKG / "libla2_trace.so" if trace else LIB
-    if not trace and not force and not _stale():
-        return LIB
-    extra, tag = (["-DLA2_TRACE"], "_trace") if trace else ((), "")
+    """Build libla2.so and libla2_dev.so (or, with trace=True, the phase-trace variant
+    libla2_trace.so). Returns the path of libla2.so."""
+    if not trace:
+        _link(DEV_LIB, DEV_SOURCES, force, verbose, (), "")
+        return _link(LIB, SOURCES, force, verbose, (), "")
+    return _link(PKG / "libla2_trace.so", SOURCES, True, verbose, ["-DLA2_TRACE"], "_trace")
+
+
+def _link(lib: Path, sources, force: bool, verbose: bool, extra, tag) -> Path:
+    if not force and not _stale(lib, sources):
+        return lib
     extra = [*extra, *os.environ.get("LA2_NVCC_EXTRA", "").split()]
-    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose, extra, tag), SOURCES))
+    with cf.ThreadPoolExecutor(len(sources)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose, extra, tag), sources))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -71,9 +71,14 @@ Workspace get_workspace(cudaStream_t st) {
 
 // Per-device side stream (non-blocking) + fork/join events for the concurrent dQ pass.
 // Fork/join through events is also valid inside CUDA graph capture.
+// The record/wait pair of each fork and join runs under the side stream's mutex, so two
+// host threads cannot interleave their records on the shared events (thread B's fork
+// record landing between thread A's record and wait would make A's side work wait on B's
+// stream instead of its own).
 struct SideStream {
   cudaStream_t s;
   cudaEvent_t fork, join;
+  std::mutex mu;
 };
 static SideStream* side_stream(cudaStream_t caller) {
   static std::mutex mu;
@@ -101,7 +106,16 @@ static SideStream* side_stream(cudaStream_t caller) {
   }
   return &per_dev[dev];
 }
+static bool fork_side(SideStream* side, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(side->mu);
+  if (cudaEventRecord(side->fork, st) == cudaSuccess &&
+      cudaStreamWaitEvent(side->s, side->fork, 0) == cudaSuccess)
+    return true;
+  cudaGetLastError();
+  return false;
+}
 static int join_side(SideStream* side, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(side->mu);
   cudaError_t e = cudaEventRecord(side->join, side->s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, side->join, 0);
   if (e != cudaSuccess) return set_cuda_error("side-stream join", e);
@@ -287,8 +301,7 @@ static int backward_impl(const void* q, const void* k, const void* v, const void
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int pair_cap = (2 * sms / 3) / 2, dq_cap = sms - 2 * pair_cap;
     SideStream* ps = (B * H > pair_cap && B * H > dq_cap) ? side_stream(st) : nullptr;
-    if (ps != nullptr && cudaEventRecord(ps->fork, st) == cudaSuccess &&
-        cudaStreamWaitEvent(ps->s, ps->fork, 0) == cudaSuccess) {
+    if (ps != nullptr && fork_side(ps, st)) {
       const int rc = backward_reverse(q, k, v, dout, decay, dk, dv, dkv_in, dkv_out, B, H, N, d,
                                       dvd, dtype, st, pair_cap, ld);
       aq.max_ranges = dq_cap;
@@ -300,12 +313,7 @@ static int backward_impl(const void* q, const void* k, const void* v, const void
   }
   SideStream* side = (tuning_value(LA2_TUNE_CONCURRENT_BWD) > 0 &&
                       N <= tuning_value(LA2_TUNE_CONCURRENT_BWD)) ? side_stream(st) : nullptr;
-  if (side != nullptr) {
-    if (cudaEventRecord(side->fork, st) != cudaSuccess || cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess) {
-      cudaGetLastError();
-      side = nullptr;
-    }
-  }
+  if (side != nullptr && !fork_side(side, st)) side = nullptr;
   if (int rc = run_f(aq, side ? side->s : st)) {
     if (side) join_side(side, st);
     return rc;
@@ -323,11 +331,6 @@ static int backward_reverse(const void* q, const void* k, const void* v, const v
                             const float* decay, void* dk, void* dv, const float* dkv_in,
                             float* dkv_out, int B, int H, int N, int d, int dvd, int dtype,
                             cudaStream_t st, int max_ranges, const long long* ld) {
-  // d = dv = 64 bf16: dK and dV in one fused reverse scan (sweep 2, kernel.py:207-231)
-  // (experimental single-kernel dK/dV scan, la2_bwd.cu; opt-in: slower than the pair below)
-  static const bool fused_g = std::getenv("LA2_FUSED_BWD_G") != nullptr;
-  if (fused_g && ld == nullptr && dtype == LA2_BF16 && d == 64 && dvd == 64)
-    return launch_g(q, k, v, dout, dk, dv, decay, dkv_in, dkv_out, B, H, N, st);
   if (dtype == LA2_BF16 && d == 64 && dvd == 64) {
     // dV and dK scans as one cluster pair sharing the Q and dO tiles (sweep 2, kernel.py:207-231)
     FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1, max_ranges};
@@ -382,6 +385,39 @@ int la2_state_scan(const float* states, const float* decay, const float* init, f
   if (int rc = bind_device(stream, states)) return rc;
   return launch_state_scan(states, decay, init, out, G, B * H, H, d, dv, lens, reverse,
                            static_cast<cudaStream_t>(stream));
+}
+
+int la2_check_decay(const float* decay, int H, void* stream) {
+  g_err[0] = 0;
+  if (decay == nullptr) return set_error(LA2_ERR_VALUE, "decay pointer is null");
+  if (H < 1) return set_error(LA2_ERR_VALUE, "H must be >= 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<float> h(static_cast<size_t>(H));
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, decay) != cudaSuccess) cudaGetLastError();
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (int rc = bind_device(stream, decay)) return rc;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return set_error(LA2_ERR_UNSUPPORTED,
+                       "la2_check_decay synchronizes the stream: call it before graph capture");
+    }
+    cudaError_t e = cudaMemcpyAsync(h.data(), decay, H * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_cuda_error("la2_check_decay", e);
+  } else {
+    std::memcpy(h.data(), decay, H * sizeof(float));
+  }
+  for (int i = 0; i < H; ++i) {
+    if (!(h[i] > 0.f && h[i] <= 1.f)) {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "decay rate must be in (0, 1], got %g (head %d)",
+                    static_cast<double>(h[i]), i);
+      return set_error(LA2_ERR_VALUE, buf);
+    }
+  }
+  return 0;
 }
 
 int la2_decode_step(const void* q, const void* k, const void* v, const float* decay, float* state,

@@ -7,6 +7,16 @@
 
 namespace la2 {
 
+#ifdef __CUDACC__
+// Decay as the kernels use it: lam in (0, 1] (reference.py:42-44), anything else
+// (including NaN) becomes NaN so that every output of the launch is NaN -- an invalid
+// decay can never produce plausible numbers. The C ABI rejects it up front with
+// la2_check_decay (include/la2.h).
+__device__ __forceinline__ float checked_decay(float lam) {
+  return (lam > 0.f && lam <= 1.f) ? lam : __int_as_float(0x7fc00000);
+}
+#endif
+
 // Arguments of one "F" pass (see la2_tc.cu header comment).
 //   q,k: [B,H,N,dk]   v,o: [B,H,N,dv]   (contiguous; o == nullptr -> state-only pass)
 //   kv_in / kv_out: fp32 [B,H,dk,dv] (kv_in_T: kv_in stored [B,H,dv,dk])
@@ -50,10 +60,6 @@ int launch_tc(const FArgs& a, cudaStream_t st);
 int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 // d = dv = 128: dV and dK reverse scans as one 4-CTA cluster per unit (two value-slice pairs).
 int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
-// Fused reverse scan of the backward pass (dK and dV together), d = dv = 64, bf16.
-int launch_g(const void* q, const void* k, const void* v, const void* dout, void* dk, void* dv,
-             const float* decay, const float* dkv_in, float* dkv_out, int B, int H, int N,
-             cudaStream_t st);
 // TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle;
 // head_stride = elements between (b, h) rows (0: N * cols).
 int tma_encoder_ready();

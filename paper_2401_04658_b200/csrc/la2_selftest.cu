@@ -1,9 +1,28 @@
 // Self-test of the tcgen05 operand layouts used by la2_tc_kernel.
 // D[M][N] = A[M][K] * B[K][N] with A staged K-major or MN-major and B staged
 // K-major or MN-major in SW128 regions, exactly as the F kernel stages Q/K/V/P/KV.
-// Used by tests/test_gpu_selftest.py; not on the product path.
+// Used by tests/test_gpu_selftest.py and tools/; not on the product path: it is built
+// into its own development library, libla2_dev.so (include/la2_dev.h), so the shipping
+// libla2.so exports only the reference-replacing ABI of include/la2.h.
+#include <cstdio>
+
+#include "../../include/la2_dev.h"
 #include "la2_kernels.h"
 #include "la2_ptx.cuh"
+
+namespace {
+thread_local char g_dev_err[256] = "";
+int dev_error(const char* msg) {
+  std::snprintf(g_dev_err, sizeof(g_dev_err), "%s", msg);
+  return LA2_ERR_VALUE;
+}
+int dev_cuda_error(const char* where, cudaError_t e) {
+  std::snprintf(g_dev_err, sizeof(g_dev_err), "%s: %s", where, cudaGetErrorString(e));
+  return LA2_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" LA2_API const char* la2_dev_last_error(void) { return g_dev_err; }
 
 namespace la2 {
 
@@ -107,15 +126,15 @@ extern "C" LA2_API int la2_selftest_umma(const float* A, const float* B, float* 
                                  int a_mn, int b_mn, void* stream) {
   using namespace la2;
   if (!((M == 64 || M == 128) && (N == 64 || N == 128) && (K == 64 || K == 128)))
-    return set_error(LA2_ERR_VALUE, "selftest: M,N in {64,128}, K in {64,128}");
+    return dev_error("selftest: M,N in {64,128}, K in {64,128}");
   const int smem = 65536 + 128 + 1024;
   cudaError_t e = cudaFuncSetAttribute(la2_umma_selftest_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda_error("selftest attr", e);
+  if (e != cudaSuccess) return dev_cuda_error("selftest attr", e);
   la2_umma_selftest_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(A, B, D, M, N, K,
                                                                                 a_mn, b_mn);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error("selftest launch", e);
+  if (e != cudaSuccess) return dev_cuda_error("selftest launch", e);
   return 0;
 }
 
@@ -180,11 +199,11 @@ extern "C" LA2_API int la2_bench_umma(int M, int N, int a_mode, int b_mn, int it
   const int smem = 65536 + 128 + 1024;
   cudaError_t e = cudaFuncSetAttribute(la2_umma_bench_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda_error("bench attr", e);
+  if (e != cudaSuccess) return dev_cuda_error("bench attr", e);
   la2_umma_bench_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(M, N, a_mode, b_mn,
                                                                                iters, out);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error("bench launch", e);
+  if (e != cudaSuccess) return dev_cuda_error("bench launch", e);
   return 0;
 }
 
@@ -232,6 +251,6 @@ extern "C" LA2_API int la2_bench_tmem(int warps, int iters, int batch, int ctas,
   la2_tmem_bench_kernel<<<ctas, warps * 32, 0, static_cast<cudaStream_t>(stream)>>>(iters, batch,
                                                                                     out, sink);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error("tmem bench launch", e);
+  if (e != cudaSuccess) return dev_cuda_error("tmem bench launch", e);
   return 0;
 }

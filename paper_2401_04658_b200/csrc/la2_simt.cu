@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(SIMT_THREADS)
   const int tid = threadIdx.x;
   if (tid == 0) {
     // iterated products with underflow flush, as tila.power_table
-    const float lam = p.decay[h];
+    const float lam = checked_decay(p.decay[h]);
     float acc = 1.f;
     bool flushed = false;
     for (int j = 0; j <= SB; ++j) {
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256)
   float* red = vs + dv;  // [256]
   const int bh = blockIdx.x;
   const int h = bh % H;
-  const float lam = decay[h];
+  const float lam = checked_decay(decay[h]);
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     qs[e] = ld_el<T>(q + static_cast<size_t>(bh) * d + e);
     ks[e] = ld_el<T>(k + static_cast<size_t>(bh) * d + e);
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256)
   __shared__ float qs[256], ks[256];
   __shared__ float4 red[256];
   const int bh = blockIdx.x, t = threadIdx.x;
-  const float lam = decay[bh % H];
+  const float lam = checked_decay(decay[bh % H]);
   if (t < d) {
     qs[t] = ld_el<T>(q + static_cast<size_t>(bh) * d + t);
     ks[t] = ld_el<T>(k + static_cast<size_t>(bh) * d + t);
@@ -342,7 +342,7 @@ __global__ void la2_scan_kernel(const float* __restrict__ states, const float* _
   const size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= total) return;
   const int bh = static_cast<int>(e / per);
-  const double l2 = log2(static_cast<double>(decay[bh % H]));
+  const double l2 = log2(static_cast<double>(checked_decay(decay[bh % H])));
   float acc = init ? init[e] : 0.f;
   if (!reverse) {
     for (int g = 0; g < G; ++g) {

@@ -19,7 +19,7 @@
 //   KV_i   = lam^r KV_{i-1} + dKV                   fp32 registers of the state warps
 // The fp32 KV state never leaves the SM.
 //
-// Warp roles (480 threads, one CTA per SM):
+// Warp roles (512 threads = 16 warps, one CTA per SM):
 //   warp 0     TMA producer (Q/K/V ring of NS stages)
 //   warp 1     MMA issuer X (S = QK^T, O = PV) + TMEM owner
 //   warp 14    MMA issuer Y (dKV = K~^T V, Oe = Q KV): the state chain never waits
@@ -27,6 +27,7 @@
 //   warps 2-9  row warps:   thread <-> token row, two warps per TMEM lane quarter
 //              splitting the columns; S -> P, O epilogue + TMA store
 //   warps 10-13 state warps: V~ rows, dKV -> fp32 KV state -> bf16 KV operand
+//   warp 15    V~ copy warp (d = 128 full passes; idle otherwise)
 //
 // Scheduling: a persistent stream-K split of the (recurrence, block) space over the
 // co-resident CTAs/clusters (Sched, la2_tc_common.cuh) when there are more recurrences
@@ -159,10 +160,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nsl = p.nsl, H = p.H, cr = static_cast<int>(prank);
   auto blk_of = [&](int pos) { return REV ? (nblk - 1 - pos) : pos; };
   // exact log2 of the head's decay (fast-math log2f is off by ~2^-22 absolute, which
-  // compounds over 64K tokens when lam is close to 1)
+  // compounds over 64K tokens when lam is close to 1); an invalid lam gives NaN
   auto log2_decay = [&](int h) {
-    const float lam = p.decay[h];
-    return (lam >= 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
+    const float lam = checked_decay(p.decay[h]);
+    return (lam == 1.f) ? 0.f : static_cast<float>(log2(static_cast<double>(lam)));
   };
 
   if (threadIdx.x == 0) {

@@ -1,5 +1,5 @@
-// Shared device-side pieces of the tcgen05 Lightning-2 kernels (F: la2_tc.cu,
-// G: la2_bwd.cu): tile constants, trace hooks, row copy/store helpers.
+// Shared device-side pieces of the tcgen05 Lightning-2 kernels (la2_tc.cu):
+// tile constants, trace hooks, row copy/store helpers.
 #pragma once
 #include "la2_kernels.h"
 #include "la2_ptx.cuh"

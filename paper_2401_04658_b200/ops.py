@@ -47,20 +47,27 @@ def _stream(dev: torch.device) -> int:
 def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
     """Per-head decay as a contiguous float32 [H] tensor on ``device``.
 
-    Host values are validated with the reference's rule lam in (0, 1]
-    (pkg/src/tila/reference.py:42-44) and raise ValueError otherwise. A CUDA
-    tensor is trusted as given (validating it would force a host sync).
+    Values are validated with the reference's rule lam in (0, 1]
+    (pkg/src/tila/reference.py:42-44) and raise ValueError otherwise: host values
+    directly, a CUDA tensor through the C ABI's ``la2_check_decay`` once per
+    (storage, version) -- the check synchronizes the stream, so repeated calls with
+    the same unmodified tensor cost nothing after the first. Inside CUDA graph
+    capture an unchecked tensor is not validated (the kernels turn an invalid lam
+    into NaN outputs, never plausible numbers).
     """
     if isinstance(decay, torch.Tensor) and decay.is_cuda:
         if (decay.dtype == torch.float32 and decay.dim() == 1 and decay.numel() == H
                 and decay.device == device and decay.is_contiguous()):
+            _check_cuda_decay(decay)
             return decay  # fast path: already a prepared per-head decay vector
         d = decay.to(device=device, dtype=torch.float32).reshape(-1)
         if d.numel() == 1:
             d = d.expand(H)
         if d.numel() != H:
             raise ValueError(f"decay must have {H} entries (one per head), got {d.numel()}")
-        return d.contiguous()
+        d = d.contiguous()
+        _check_cuda_decay(d)
+        return d
     if isinstance(decay, torch.Tensor):
         vals = decay.detach().double().reshape(-1).tolist()
     elif isinstance(decay, (int, float)):
@@ -78,6 +85,21 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
 
 
 _DECAY_CACHE: dict = {}
+_CHECKED: dict = {}  # (data_ptr, numel, device) -> tensor version last validated
+
+
+def _check_cuda_decay(d: torch.Tensor) -> None:
+    """la2_check_decay on a contiguous float32 CUDA decay vector, once per version."""
+    key = (d.data_ptr(), d.numel(), d.device.index)
+    ver = d._version
+    if _CHECKED.get(key) == ver:
+        return
+    if torch.cuda.is_current_stream_capturing():
+        return  # cannot synchronize inside capture; the kernels poison invalid lam with NaN
+    _lib.call("la2_check_decay", d.data_ptr(), d.numel(), _stream(d.device))
+    if len(_CHECKED) >= 1024:
+        _CHECKED.clear()
+    _CHECKED[key] = ver
 
 
 def _decay(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
@@ -135,6 +157,7 @@ def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name) -> Optional[tor
 
 # ------------------------------------------------------ intra-GPU sequence split
 NUM_SMS = 148
+MAX_CHUNKS = 64  # la2_state_scan combines at most 64 chunk states per call
 
 
 def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
@@ -156,7 +179,8 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     if dtype == torch.bfloat16 and d in (64, 128) and dv % 64 == 0:
         if units >= 100:
             return 1
-        while units * g < NUM_SMS and N % (2 * g * 128) == 0 and N // (2 * g) >= 8192:
+        while (units * g < NUM_SMS and 2 * g <= MAX_CHUNKS and N % (2 * g * 128) == 0
+               and N // (2 * g) >= 8192):
             g *= 2
         # each pass of a split runs over N/g tokens serially plus fixed launch/ramp costs,
         # so a 2-way split never pays (tools/bf16_split.py)
@@ -164,7 +188,7 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     if d > 256 or dv > 256:
         return 1
     min_chunk = 32 if max(d, dv) <= 64 else 128
-    while units * g < 4 * NUM_SMS and 2 * g <= 64 and N % (2 * g) == 0 and N // (2 * g) >= min_chunk:
+    while units * g < 4 * NUM_SMS and 2 * g <= MAX_CHUNKS and N % (2 * g) == 0 and N // (2 * g) >= min_chunk:
         g *= 2
     return g
 

@@ -2,7 +2,9 @@
 
 Same names, argument meaning and error behaviour as the reference ``tila``
 package (pkg/src/tila/__init__.py:13-40), so the reference's own test cases
-run unchanged against this module:
+run against this module (results agree to the fp32 tolerance, not bitwise: the
+GPU picks its own tile, so e.g. the reference's "block-aligned chunks are
+bitwise equal" property holds only for the GPU's own block size):
 
   tiled_forward(q, k, v, lam, block)            pkg/src/tila/kernel.py:122-139
   chunked_forward(q, k, v, lam, block, state)   pkg/src/tila/kernel.py:142-162
@@ -176,12 +178,14 @@ def _backward_group(heads):
 
 
 def _batched(inputs, block, fn, ncheck):
-    _check_block(block)
+    # per head, in the reference's order (inputs, decay, block: kernel.py:122-139), so an
+    # error reads "head i: ..." and an empty input list returns [] whatever the block
     checked = []
     for i, item in enumerate(inputs):
         try:
             arrs = _check_inputs(*item[:ncheck])
             _check_decay(item[ncheck])
+            _check_block(block)
         except Exception as exc:  # same re-raise as kernel.py:236-240
             raise type(exc)(f"head {i}: {exc}") from exc
         checked.append((*arrs, item[ncheck]))

@@ -100,3 +100,31 @@ def test_header_is_plain_c_and_links(lib, tmp_path):
                     f"-L{libdir}", "-l:libla2.so", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     res = subprocess.run([str(exe)], capture_output=True, text=True)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+def test_check_decay_host_memory(lib):
+    """la2_check_decay on host memory needs no device: lam in (0, 1] passes, anything
+    else is LA2_ERR_VALUE naming the head (reference.py:42-44)."""
+    from paper_2401_04658_b200 import _lib
+
+    good = (ctypes.c_float * 3)(0.5, 1.0, 1e-30)
+    assert lib.la2_check_decay(good, 3, None) == 0
+    for vals in ((0.5, 1.5), (0.5, 0.0), (0.5, -1.0), (0.5, float("nan"))):
+        arr = (ctypes.c_float * 2)(*vals)
+        assert lib.la2_check_decay(arr, 2, None) == _lib.LA2_ERR_VALUE
+        assert b"head 1" in lib.la2_last_error()
+    assert lib.la2_check_decay(None, 2, None) == _lib.LA2_ERR_VALUE
+
+
+def test_dev_library_is_separate(lib):
+    """The self-test / micro-benchmark entry points live in libla2_dev.so
+    (include/la2_dev.h), not in the shipping libla2.so."""
+    from paper_2401_04658_b200 import _lib
+
+    dev = _lib.load_dev()
+    text = (ROOT / "include" / "la2_dev.h").read_text()
+    dev_syms = set(re.findall(r"LA2_API\s+[\w\s\*]+?\b(la2_\w+)\s*\(", text))
+    assert dev_syms == set(_lib.DEV_SIGNATURES)
+    for name in dev_syms:
+        assert hasattr(dev, name), name
+        assert not hasattr(lib, name), name

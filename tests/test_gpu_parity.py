@@ -646,29 +646,50 @@ def test_random_shapes_against_oracle(case):
     assert max(errs.values()) <= BF16_TOL, ((B, H, N, d, dv), errs)
 
 
-def test_fused_g_backward_opt_in():
-    """The single-CTA fused dK/dV scan (la2_bwd.cu, opt-in with LA2_FUSED_BWD_G; slower than
-    the cluster pair) still matches the oracle -- run in a subprocess so the env applies."""
-    import subprocess
-    import sys
-    from pathlib import Path
-    code = (
-        "import numpy as np, torch, paper_2401_04658_b200 as la2\n"
-        "from oracle import tila_port as port\n"
-        "g = torch.Generator().manual_seed(4)\n"
-        "q, k, v, do = ((torch.rand(2, 3, 700, 64, generator=g) * 2 - 1).bfloat16() for _ in range(4))\n"
-        "decay = [0.9, 0.999, 1.0]\n"
-        "dq, dk, dv, _ = la2.la2_backward(*(t.cuda() for t in (q, k, v, do)), decay)\n"
-        "Q, K, V, DO = (t.double().numpy() for t in (q, k, v, do))\n"
-        "rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)\n"
-        "e = max(port.rel_err(a.double().cpu().numpy(), b) for a, b in ((dq, rq), (dk, rk), (dv, rv)))\n"
-        "assert e <= 1e-2, e\n"
-        "print('ok', e)\n")
-    root = Path(__file__).resolve().parents[1]
-    env = dict(__import__("os").environ, LA2_FUSED_BWD_G="1")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+def test_invalid_cuda_decay_raises_value_error():
+    """A CUDA decay tensor outside (0, 1] raises ValueError like the reference's
+    _check_decay (pkg/src/tila/reference.py:42-44), through every op."""
+    from paper_2401_04658_b200 import ops
+    q, k, v = (torch.rand(1, 2, 256, 64, device=DEV).bfloat16() for _ in range(3))
+    for bad in ([0.9, 1.5], [0.0, 0.5], [-0.1, 0.5], [float("nan"), 0.5]):
+        dec = torch.tensor(bad, device=DEV)
+        with pytest.raises(ValueError, match=r"decay rate must be in \(0, 1\]"):
+            la2.lightning_attn2(q, k, v, dec)
+        with pytest.raises(ValueError):
+            ops.la2_forward(q, k, v, dec)
+        with pytest.raises(ValueError):
+            ops.chunk_state(k, v, dec)
+    # a valid tensor passes, and is validated again after an in-place change
+    dec = torch.tensor([0.9, 1.0], device=DEV)
+    la2.lightning_attn2(q, k, v, dec)
+    dec.fill_(2.0)
+    with pytest.raises(ValueError):
+        la2.lightning_attn2(q, k, v, dec)
+
+
+def test_invalid_decay_poisons_outputs_in_kernels():
+    """Below the validation layer (raw C ABI, e.g. inside graph capture) the kernels never
+    clamp an invalid lam: every output of that head is NaN, the valid head is unaffected."""
+    from paper_2401_04658_b200 import _lib
+    for dt, d in ((torch.bfloat16, 64), (torch.bfloat16, 128), (torch.float32, 64), (torch.bfloat16, 32)):
+        q, k, v = (torch.rand(1, 2, 300, d, device=DEV).to(dt) for _ in range(3))
+        o = torch.empty_like(v)
+        dec = torch.tensor([1.5, 0.9], device=DEV)
+        code = _lib.LA2_BF16 if dt == torch.bfloat16 else _lib.LA2_FP32
+        _lib.call("la2_forward", q.data_ptr(), k.data_ptr(), v.data_ptr(), dec.data_ptr(), o.data_ptr(),
+                  None, None, 1, 2, 300, d, d, code, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.isnan(o[0, 0]).all(), (dt, d)
+        assert torch.isfinite(o[0, 1]).all(), (dt, d)
+
+
+def test_check_decay_abi():
+    from paper_2401_04658_b200 import _lib
+    good = torch.tensor([0.5, 1.0, 1e-30], device=DEV)
+    _lib.call("la2_check_decay", good.data_ptr(), 3, torch.cuda.current_stream().cuda_stream)
+    bad = torch.tensor([0.5, 1.0000001], device=DEV)
+    with pytest.raises(ValueError, match="head 1"):
+        _lib.call("la2_check_decay", bad.data_ptr(), 2, torch.cuda.current_stream().cuda_stream)
 
 
 def test_host_decay_upload_cached():

@@ -24,7 +24,7 @@ def test_umma_layouts(M, N, K, a_mn, b_mn):
     B = (torch.rand(K, N, generator=g) * 2 - 1).bfloat16().float()
     Ad, Bd = A.cuda(), B.cuda()
     D = torch.full((M, N), float("nan"), device="cuda")
-    _lib.call("la2_selftest_umma", Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn,
+    _lib.call_dev("la2_selftest_umma", Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn,
               torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     ref = A.double() @ B.double()

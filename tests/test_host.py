@@ -85,6 +85,12 @@ def test_split_factor_policy():
     assert split_factor(1, 1, 1 << 20, 64, 64, torch.float32) == 64       # scan limit
     assert split_factor(1, 3, 333, 4, 7, torch.float32) == 1              # odd length
     assert split_factor(64, 16, 4096, 64, 64, torch.float32) == 1         # already 1024 units
+    # long few-head sequences: never more chunks than la2_state_scan combines (64)
+    for shape in ((1, 1, 1 << 20, 64, 64), (1, 2, 1 << 20, 64, 64), (1, 1, 1 << 20, 128, 128),
+                  (1, 2, 1 << 20, 128, 128), (1, 1, 1 << 21, 64, 64), (1, 1, 1 << 23, 128, 128)):
+        g = split_factor(*shape, torch.bfloat16)
+        assert 1 <= g <= 64 and shape[2] % g == 0, (shape, g)
+    assert split_factor(1, 1, 1 << 21, 64, 64, torch.bfloat16) == 64
 
 
 def test_gpubench_verdict_and_csv(tmp_path):

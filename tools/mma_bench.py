@@ -11,7 +11,7 @@ for ctas in (1, 148):
     for M, N, am, bm, ch in cfgs:
         out = torch.zeros(ctas, dtype=torch.int64, device='cuda')
         for _ in range(2):
-            _lib.call("la2_bench_umma", M, N, am, bm | (ch << 1), iters, ctas, out.data_ptr(), 0)
+            _lib.call_dev("la2_bench_umma", M, N, am, bm | (ch << 1), iters, ctas, out.data_ptr(), 0)
         torch.cuda.synchronize()
         cyc = out.float().mean().item() / iters
         print(f"ctas={ctas} M={M} N={N} a_mode={am} b_mn={bm} chains={ch}: {cyc:.1f} cyc/mma  "

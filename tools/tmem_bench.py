@@ -9,7 +9,7 @@ for warps in (4, 8, 16):
         out = torch.zeros(ctas, dtype=torch.int64, device='cuda')
         sink = torch.zeros(ctas * warps * 32, device='cuda')
         for _ in range(2):
-            _lib.call("la2_bench_tmem", warps, iters, batch, ctas, out.data_ptr(), sink.data_ptr(), 0)
+            _lib.call_dev("la2_bench_tmem", warps, iters, batch, ctas, out.data_ptr(), sink.data_ptr(), 0)
         torch.cuda.synchronize()
         cyc = out.float().mean().item()
         total = warps * iters * 32 * 64  # bytes per SM
