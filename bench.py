@@ -61,19 +61,6 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def load_traffic(tokens_heads: int):
-    """DRAM bytes of one forward F launch, from the committed ncu --set full capture
-    (profiles/ncu_summary.json: dram read+write per token-head), scaled to B*H*N."""
-    p = ROOT / "profiles" / "ncu_summary.json"
-    if p.exists():
-        try:
-            j = json.loads(p.read_text())
-            return j["fwd_dram_bytes_per_token_head"] * tokens_heads
-        except Exception:
-            pass
-    return None
-
-
 class ClockSampler:
     """SM clocks + throttle reasons sampled every 20 ms through NVML while the
     timed region runs (falls back to nvidia-smi if pynvml is unavailable)."""
@@ -231,6 +218,73 @@ def c5_phases(q, k, v, do, dec, world, timed_phase):
     return res
 
 
+def _oracle_head_task(args):
+    """fp64 tiled forward + backward of one head (the pinned oracle port, block 64)."""
+    q, k, v, do, lam = args
+    from oracle import tila_port as port
+
+    o, _ = port.tiled_forward(q, k, v, lam, 64)
+    g = port.tiled_backward(q, k, v, do, lam, 64)
+    return o, g.dq, g.dk, g.dv
+
+
+def parity_spot_check(heads, tol=1e-2):
+    """heads: list of (label, lam, q, k, v, do, o, dq, dk, dv) numpy arrays of one head, the
+    inputs as the GPU saw them (bf16 values) and the GPU outputs. Compares against the fp64
+    oracle with the reference's metric (verify.py:50-75) in a process pool."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    from oracle import tila_port as port
+
+    tasks = [(h[2], h[3], h[4], h[5], h[1]) for h in heads]
+    with cf.ProcessPoolExecutor(max_workers=len(tasks), mp_context=mp.get_context("spawn")) as ex:
+        refs = list(ex.map(_oracle_head_task, tasks))
+    rows = []
+    for h, ref in zip(heads, refs):
+        errs = {n: port.rel_err(got, r) for n, got, r in zip(("o", "dq", "dk", "dv"), h[6:10], ref)}
+        rows.append({"head": h[0], "lam": h[1], "rel_err": errs})
+    worst = max(max(r["rel_err"].values()) for r in rows)
+    return {"oracle": "oracle/tila_port.py tiled fp64 (block 64) on the same bf16 inputs",
+            "metric": "max|gpu-ref|/max|ref| (verify.py:50-75)", "tol": tol, "heads": rows,
+            "max_rel_err": worst, "pass": bool(worst <= tol)}
+
+
+def launch_roles(recs, roles):
+    """Group a launch log by role: recs is the log of `steps` calls whose per-call launch
+    pattern is roles (a list of role names, one per launch of one call)."""
+    out = {}
+    if not recs or len(recs) % len(roles):
+        return out
+    for i, r in enumerate(recs):
+        role = roles[i % len(roles)]
+        e = out.setdefault(role, {"kernel": r["kernel"], "grid": r["grid"], "cluster": r["cluster"],
+                                  "ms": []})
+        e["ms"].append(r["ms"])
+    for e in out.values():
+        e["ms"] = statistics.median(e["ms"])
+    return out
+
+
+def load_ncu_bytes(d: int):
+    """DRAM bytes per (token, head) of each launch of one fwd+bwd step (forward F, dQ F,
+    dK/dV pair) from the committed ncu --set full capture (profiles/ncu_summary.json)."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        j = json.loads(p.read_text())
+        key = f"full_d{d}"
+        th = j["token_heads"][key]
+        ls = j["launches"][key]
+        if len(ls) != 3:
+            return None
+        return {role: (x["dram_read_bytes"] + x["dram_write_bytes"]) / th
+                for role, x in zip(("forward", "dq", "dkdv"), ls)}
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -241,9 +295,12 @@ def main():
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--dim", type=int, default=64)
     ap.add_argument("--seq-len", type=int, default=65536)
+    ap.add_argument("--soak-s", type=float, default=1.0,
+                    help="seconds of back-to-back steps before the timed (sustained) steps")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=48)
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c2 (default) = the headline BASELINE configs[1]; c1/c3/c4/c5 = the other configs")
@@ -259,7 +316,8 @@ def main():
               "batch_per_gpu": B, "global_batch": B * world, "heads": H, "head_dim": D,
               "seq_len": N, "decay": "alibi-style exp(-2^(-8(h+1)/H))",
               "parallelism": f"bxh-shard x{world}" if world > 1 else "single",
-              "l2": "inputs (1 GiB/tensor at N=64K) larger than L2; no flush"}
+              "l2": "inputs (1 GiB/tensor at N=64K) larger than L2; no flush",
+              "timing": f"sustained: {args.soak_s:g} s of back-to-back steps, then the K timed steps"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -278,12 +336,14 @@ def main():
     import torch.distributed as dist
 
     import paper_2401_04658_b200 as la2
+    from paper_2401_04658_b200 import ops
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    decay = la2.decay_tensor(alibi_decay(H), H, dev)
+    lams = alibi_decay(H)
+    decay = la2.decay_tensor(lams, H, dev)
 
     def make(n, seed):
         g = torch.Generator(device=dev).manual_seed(seed + 1000 * rank)
@@ -305,11 +365,9 @@ def main():
         la2.la2_forward(q, k, v, decay)
         la2.la2_backward(q, k, v, do, decay)
 
-    def time_steps(fn, steps, warmup):
-        for _ in range(warmup):
-            fn()
-        barrier()
-        torch.cuda.synchronize()
+    def run_timed(fn, steps):
+        """Device time per call of `steps` back-to-back calls (events on torch's current
+        stream, which is the stream the library launches on)."""
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
@@ -317,39 +375,115 @@ def main():
             fn()
         e1.record(st)
         torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    def time_steps(fn, steps, warmup, soak_s=0.0):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        soak = None
+        if soak_s > 0:
+            # bring the board to its steady state (power limit) before the timed steps
+            probe = run_timed(fn, 2)
+            n_soak = max(4, int(math.ceil(soak_s * 1e3 / max(probe, 1e-3))))
+            soak = {"steps": n_soak, "ms_per_step": run_timed(fn, n_soak)}
+            soak["window_s"] = soak["ms_per_step"] * n_soak / 1e3
         barrier()
-        return max_over_ranks(e0.elapsed_time(e1) / steps)
+        torch.cuda.synchronize()
+        ms = run_timed(fn, steps)
+        barrier()
+        return max_over_ranks(ms), soak
 
     hbm_peak, tc_peak, peak_src = load_peaks()
+    ff, fb = canonical_flops(N, D, D)
+    bf, bb = canonical_bytes(N, D, D)
 
-    # ---------------- headline: fwd+bwd at N
+    # ---------------- burst: K steps on a rested GPU (reported beside the headline)
     q, k, v, do = make(N, 0)
+    ms_burst, _ = time_steps(lambda: step(q, k, v, do), args.steps, max(3, args.warmup))
+
+    # ---------------- per-launch times (launch log: events on the launching stream)
+    # in the sustained regime, like the headline
+    time_steps(lambda: step(q, k, v, do), 0, 0, soak_s=args.soak_s)
+    ops.launch_log(4 * max(3, args.steps) + 8)
+    for _ in range(max(3, args.steps)):
+        la2.la2_forward(q, k, v, decay)
+    fwd_log = ops.read_launch_log()
+    for _ in range(max(3, args.steps)):
+        la2.la2_backward(q, k, v, do, decay)
+    bwd_log = ops.read_launch_log()
+    ops.launch_log(0)
+    n_f = max(3, args.steps)
+    per_call_f, per_call_b = len(fwd_log) // n_f, len(bwd_log) // n_f
+    roles = launch_roles(fwd_log, ["forward"] * per_call_f if per_call_f == 1 else
+                         [f"forward{i}" for i in range(per_call_f)])
+    roles.update(launch_roles(bwd_log, ["dq", "dkdv"] if per_call_b == 2 else
+                              [f"backward{i}" for i in range(per_call_b)]))
+    launches_per_step = per_call_f + per_call_b
+
+    # ---------------- headline: sustained (soak, then exactly K timed steps)
     clocks = ClockSampler(local_rank).start()
-    ms = time_steps(lambda: step(q, k, v, do), args.steps, max(3, args.warmup))
+    ms, soak = time_steps(lambda: step(q, k, v, do), args.steps, max(3, args.warmup), soak_s=args.soak_s)
     clk = clocks.stop()
     tokens_step = B * N * world
     value = tokens_step / (ms / 1e3)
-    ff, fb = canonical_flops(N, D, D)
-    bf, bb = canonical_bytes(N, D, D)
     tflops = (ff + fb) * B * H * world / (ms / 1e3) / 1e12
     t_roof = max((ff + fb) * B * H / (tc_peak * 1e12), (bf + bb) * B * H / (hbm_peak * 1e9)) * 1e3
 
-    # ---------------- dominant kernel: the F kernel, timed alone (forward launch)
-    ms_fwd = time_steps(lambda: la2.la2_forward(q, k, v, decay), max(3, args.steps), 2)
-    ms_bwd = time_steps(lambda: la2.la2_backward(q, k, v, do, decay), max(3, args.steps), 2)
-    fwd_bytes = bf * B * H
-    achieved = fwd_bytes / (ms_fwd / 1e3) / 1e9
-    traffic = load_traffic(B * H * N)
-    roofline = {"bound": "hbm", "kernel": "la2_tc_kernel<64,fwd> (one F launch = the forward pass)",
-                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "peak_source": peak_src, "algorithmic_bytes_per_launch": fwd_bytes,
-                "traffic": traffic,
-                "launch_ms": ms_fwd,
+    # ---------------- roofline per launch; the dominant kernel is the one with the largest share
+    e = 2
+    alg = {"forward": B * H * N * e * (2 * D + 2 * D),   # read q, k, v; write o
+           "dq": B * H * N * e * (2 * D + 2 * D),        # read dO, V, K; write dQ
+           "dkdv": B * H * N * e * (3 * D + 3 * D)}      # read K, Q, dO, V; write dK, dV
+    ncu_bytes = load_ncu_bytes(D)
+    launches = []
+    for role, r in roles.items():
+        a_bytes = alg.get(role)
+        ent = {"role": role, "kernel": r["kernel"], "grid": r["grid"], "cluster": r["cluster"],
+               "launch_ms": r["ms"]}
+        if a_bytes:
+            ach = a_bytes / (r["ms"] / 1e3) / 1e9
+            ent.update({"algorithmic_bytes": a_bytes, "achieved_gbs": ach, "frac": ach / hbm_peak,
+                        "traffic": (ncu_bytes[role] * B * H * N) if ncu_bytes else None})
+        launches.append(ent)
+    sum_launch = sum(x["launch_ms"] for x in launches) or 1.0
+    for x in launches:
+        x["share_of_step"] = x["launch_ms"] / sum_launch
+    dom = max(launches, key=lambda x: x["launch_ms"]) if launches else None
+    step_alg = (bf + bb) * B * H
+    step_traffic = sum(ncu_bytes.values()) * B * H * N if ncu_bytes else None
+    roofline = {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "peak_source": peak_src,
+                "kernel": dom and dom["kernel"], "role": dom and dom["role"],
+                "achieved": dom and dom.get("achieved_gbs"), "frac": dom and dom.get("frac"),
+                "algorithmic_bytes_per_launch": dom and dom.get("algorithmic_bytes"),
+                "traffic": dom and dom.get("traffic"), "launch_ms": dom and dom["launch_ms"],
+                "launches": launches,
                 "step": {"t_roof_ms": t_roof, "t_ms": ms, "frac_of_roof": t_roof / ms,
                          "tflops": tflops, "frac_of_bf16_peak": tflops / tc_peak,
-                         "fwd_ms": ms_fwd, "bwd_ms": ms_bwd}}
+                         "algorithmic_bytes": step_alg, "dram_bytes_ncu": step_traffic,
+                         "traffic_ratio": (step_traffic / step_alg) if step_traffic else None,
+                         "sum_of_launches_ms": sum_launch},
+                "note": "per-launch times from the library's launch log (CUDA events on the launching "
+                        "stream, sustained regime); traffic = ncu dram read+write per token-head "
+                        "(profiles/ncu_summary.json) scaled to this shape"}
 
-    # ---------------- sweep 1K..64K
+    # ---------------- parity spot check of the timed configuration (two heads)
+    parity = None
+    if not args.no_parity and rank == 0:
+        qg, kg, vg = (t.detach().clone().requires_grad_() for t in (q, k, v))
+        o = la2.lightning_attn2(qg, kg, vg, decay)
+        o.backward(do)
+        torch.cuda.synchronize()
+        picks = [(0, 0), (B - 1, H - 1)]
+        heads = []
+        for b, h in picks:
+            f64 = lambda t: t[b, h].detach().double().cpu().numpy()  # noqa: E731
+            heads.append((f"b{b}h{h}", lams[h], f64(q), f64(k), f64(v), f64(do), f64(o), f64(qg.grad),
+                          f64(kg.grad), f64(vg.grad)))
+        del qg, kg, vg, o
+        parity = parity_spot_check(heads)
+
+    # ---------------- sweep 1K..64K, each point in the same sustained regime
     sweep = []
     if not args.no_sweep:
         del q, k, v, do
@@ -358,7 +492,7 @@ def main():
         while n <= N:
             qs, ks, vs, dos = make(n, n)
             reps = max(5, min(50, (1 << 22) // n))
-            t = time_steps(lambda: step(qs, ks, vs, dos), reps, 3)
+            t, _ = time_steps(lambda: step(qs, ks, vs, dos), reps, 3, soak_s=args.soak_s)
             fwdf, bwdf = canonical_flops(n, D, D)
             sweep.append({"seq_len": n, "ms": t, "tokens_per_s": B * n * world / (t / 1e3),
                           "tflops": (fwdf + bwdf) * B * H * world / (t / 1e3) / 1e12,
@@ -373,19 +507,24 @@ def main():
     else:
         flat = None
 
-    # ---------------- e2e through the public API with host buffers
+    # ---------------- e2e through the public API: pinned host inputs in, o and the
+    # gradients back to pinned host buffers, every step
     e2e = None
     if not args.no_e2e:
         host = [t.cpu().pin_memory() for t in make(N, 7)]
         h2d = sum(t.numel() * t.element_size() for t in host)
+        outs = [torch.empty_like(host[0]).pin_memory() for _ in range(4)]
+        d2h = sum(t.numel() * t.element_size() for t in outs)
 
         def e2e_step():
             qh, kh, vh, doh = (t.to(dev, non_blocking=True) for t in host)
             qh.requires_grad_(); kh.requires_grad_(); vh.requires_grad_()
             o = la2.lightning_attn2(qh, kh, vh, decay)
-            loss = (o.float() * doh.float()).sum()
-            loss.backward()
-            return loss.item()
+            outs[0].copy_(o.detach(), non_blocking=True)
+            o.backward(doh)
+            for dst, src in zip(outs[1:], (qh.grad, kh.grad, vh.grad)):
+                dst.copy_(src, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
 
         for _ in range(2):
             e2e_step()
@@ -398,23 +537,31 @@ def main():
         torch.cuda.synchronize()
         barrier()
         t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+        pcie = (h2d + d2h) / t_e2e / 1e9
         e2e = {"value": tokens_step / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 4, "ms_per_step": t_e2e * 1e3,
-               "api": "paper_2401_04658_b200.lightning_attn2 autograd fwd+bwd, pinned host inputs"}
+               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+               "host_link_gbs": pcie,
+               "bound": f"host link: {(h2d + d2h) / 2**30:.1f} GiB per step at {pcie:.0f} GB/s "
+                        f"vs {ms:.2f} ms of device time",
+               "api": "paper_2401_04658_b200.lightning_attn2 autograd fwd+bwd; q,k,v,dO from pinned "
+                      "host, o,dq,dk,dv back to pinned host"}
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
-        cb = cpu_reference(N, D, B * H, B * N, args.cpu_sample_heads)
+        cb = cpu_reference(N, D, B * H, B * N, args.cpu_sample_heads, reps=3)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
-    # our kernels per timed step: forward F, dQ F, dK/dV cluster pair (la2_backward)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": config, "tflops": tflops, "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": 3 * args.steps, "clocks": clk,
+                "config": config, "tflops": tflops,
+                "burst": {"ms_per_step": ms_burst, "tokens_per_s": tokens_step / (ms_burst / 1e3),
+                          "note": "K steps on a rested GPU (before the power soak)"},
+                "sustained_window": soak,
+                "roofline": roofline, "parity": parity, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk,
                 "sweep": sweep, "flatness": flat}
         print(json.dumps(line))
     if world > 1:

@@ -195,6 +195,24 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
 #define LA2_TUNE_PDL 7
 LA2_API int la2_set_tuning(int key, int value);
 
+/*
+ * Launch log (instrumentation; not a reference interface). la2_launch_log(capacity)
+ * preallocates `capacity` event pairs and starts recording: every kernel launch of the
+ * library is then bracketed by two CUDA events recorded on the stream it is launched
+ * on (launches inside graph capture are not logged). la2_launch_log_read() waits for
+ * the logged launches, copies up to max_records of them (in launch order) and resets
+ * the log; it returns the number copied or a negative status. capacity 0 stops
+ * logging and frees the events. Used by bench.py for the per-kernel roofline.
+ */
+typedef struct la2_launch_record {
+  char kernel[48]; /* e.g. "la2_tc_kernel<64,1,0,2>" (the ncu kernel name) */
+  int grid;        /* CTAs launched */
+  int cluster;     /* CTAs per cluster */
+  float ms;        /* event-timed duration on the launching stream */
+} la2_launch_record;
+LA2_API int la2_launch_log(int capacity);
+LA2_API int la2_launch_log_read(la2_launch_record* out, int max_records);
+
 /* Bytes of the per-(device, stream) workspace on the current device (0 without a
  * device). Constant in B, H, N: the working set of a pass is independent of the
  * sequence length (the reference's constant-scratch property, scratch.py /

@@ -24,6 +24,13 @@ LA2_ERR_CUDA = -3
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
 
+
+class LaunchRecord(ctypes.Structure):
+    """struct la2_launch_record (include/la2.h)."""
+    _fields_ = [("kernel", ctypes.c_char * 48), ("grid", ctypes.c_int), ("cluster", ctypes.c_int),
+                ("ms", ctypes.c_float)]
+
+
 # name -> argtypes (restype int unless listed in _RESTYPES)
 SIGNATURES: dict[str, list] = {
     "la2_version": [],
@@ -39,6 +46,8 @@ SIGNATURES: dict[str, list] = {
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_check_decay": [_vp, _i, _vp],
+    "la2_launch_log": [_i],
+    "la2_launch_log_read": [ctypes.POINTER(LaunchRecord), _i],
     "la2_set_tuning": [_i, _i],
     "la2_workspace_bytes": [],
 }

@@ -3,6 +3,7 @@
 // selection, and the backward pass expressed as three F passes.
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -67,6 +68,48 @@ Workspace get_workspace(cudaStream_t st) {
   Workspace w{static_cast<float*>(buf), flags, slots};
   cache.push_back(Entry{dev, st, w});
   return w;
+}
+
+// ------------------------------------------------------------------ launch log
+struct LogRec {
+  char kernel[48];
+  int grid, cluster;
+  cudaEvent_t t0, t1;
+};
+static std::atomic<int> g_log_on{0};
+static std::mutex g_log_mu;
+static std::vector<LogRec> g_log;  // events preallocated by la2_launch_log
+static int g_log_used = 0, g_log_dropped = 0;
+
+LaunchScope::LaunchScope(cudaStream_t s, const char* kernel, int grid, int cluster) {
+  if (!g_log_on.load(std::memory_order_relaxed)) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;  // events inside a captured graph would time the capture, not the replay
+  }
+  std::lock_guard<std::mutex> lock(g_log_mu);
+  if (g_log_used >= static_cast<int>(g_log.size())) {
+    ++g_log_dropped;
+    return;
+  }
+  LogRec& r = g_log[g_log_used];
+  std::snprintf(r.kernel, sizeof(r.kernel), "%s", kernel);
+  r.grid = grid;
+  r.cluster = cluster;
+  if (cudaEventRecord(r.t0, s) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  slot = g_log_used++;
+  st = s;
+}
+
+LaunchScope::~LaunchScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lock(g_log_mu);
+  if (slot < static_cast<int>(g_log.size()) && cudaEventRecord(g_log[slot].t1, st) != cudaSuccess)
+    cudaGetLastError();
 }
 
 // Per-device side stream (non-blocking) + fork/join events for the concurrent dQ pass.
@@ -385,6 +428,53 @@ int la2_state_scan(const float* states, const float* decay, const float* init, f
   if (int rc = bind_device(stream, states)) return rc;
   return launch_state_scan(states, decay, init, out, G, B * H, H, d, dv, lens, reverse,
                            static_cast<cudaStream_t>(stream));
+}
+
+int la2_launch_log(int capacity) {
+  g_err[0] = 0;
+  if (capacity < 0) return set_error(LA2_ERR_VALUE, "capacity must be >= 0");
+  std::lock_guard<std::mutex> lock(g_log_mu);
+  g_log_on.store(0);
+  for (LogRec& r : g_log) {
+    cudaEventDestroy(r.t0);
+    cudaEventDestroy(r.t1);
+  }
+  g_log.clear();
+  g_log_used = g_log_dropped = 0;
+  if (capacity == 0) return 0;
+  g_log.resize(static_cast<size_t>(capacity));
+  for (LogRec& r : g_log) {
+    cudaError_t e = cudaEventCreate(&r.t0);
+    if (e == cudaSuccess) e = cudaEventCreate(&r.t1);
+    if (e != cudaSuccess) {
+      g_log.clear();
+      return set_cuda_error("la2_launch_log: cudaEventCreate", e);
+    }
+  }
+  g_log_on.store(1);
+  return 0;
+}
+
+int la2_launch_log_read(la2_launch_record* out, int max_records) {
+  g_err[0] = 0;
+  std::lock_guard<std::mutex> lock(g_log_mu);
+  const int n = g_log_used < max_records ? g_log_used : max_records;
+  for (int i = 0; i < n; ++i) {
+    LogRec& r = g_log[i];
+    cudaError_t e = cudaEventSynchronize(r.t1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.t0, r.t1);
+    if (e != cudaSuccess) return set_cuda_error("la2_launch_log_read", e);
+    std::snprintf(out[i].kernel, sizeof(out[i].kernel), "%s", r.kernel);
+    out[i].grid = r.grid;
+    out[i].cluster = r.cluster;
+    out[i].ms = ms;
+  }
+  const int dropped = g_log_dropped + (g_log_used - n);
+  g_log_used = 0;
+  g_log_dropped = 0;
+  (void)dropped;
+  return n;
 }
 
 int la2_check_decay(const float* decay, int H, void* stream) {

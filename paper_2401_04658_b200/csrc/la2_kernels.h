@@ -80,6 +80,16 @@ struct Workspace {
 };
 Workspace get_workspace(cudaStream_t st);
 
+// Launch log (la2_launch_log, include/la2.h): when enabled, every kernel launch of the
+// library is bracketed by CUDA events recorded on the stream it is launched on. A scope
+// object around the launch; free when the log is off (one relaxed load).
+struct LaunchScope {
+  int slot = -1;
+  cudaStream_t st = nullptr;
+  LaunchScope(cudaStream_t s, const char* kernel, int grid, int cluster);
+  ~LaunchScope();
+};
+
 int set_tuning(int key, int value);
 int tuning_value(int key);
 int set_error(int code, const char* msg);

@@ -163,6 +163,7 @@ int launch_simt(const FArgs& a, cudaStream_t st) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
                              static_cast<int>(smem));                                             \
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(simt)", e);                 \
+    LaunchScope log_scope(st, "la2_simt_kernel<" #TY "," #RV ">", nslices * a.H * a.B, 1);      \
     kern<<<grid, SIMT_THREADS, smem, st>>>(static_cast<const TY*>(a.q), static_cast<const TY*>(a.k), \
                                            static_cast<const TY*>(a.v), static_cast<TY*>(a.o), p, \
                                            a.dk, dvs);                                            \
@@ -306,6 +307,7 @@ static bool launch_decode_vec(const void* q, const void* k, const void* v, const
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st) {
   if (dv > 256) return set_error(LA2_ERR_UNSUPPORTED, "decode supports dv <= 256");
+  LaunchScope log_scope(st, "la2_decode_kernel", B * H, 1);
   const bool vec = (dtype == LA2_FP32)
                        ? launch_decode_vec<float>(q, k, v, decay, state, o, B, H, d, dv, st)
                        : launch_decode_vec<__nv_bfloat16>(q, k, v, decay, state, o, B, H, d, dv, st);
@@ -374,6 +376,7 @@ int launch_state_scan(const float* states, const float* decay, const float* init
   const size_t total = static_cast<size_t>(BH) * per;
   const int threads = 256;
   const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
+  LaunchScope log_scope(st, "la2_scan_kernel", static_cast<int>(blocks), 1);
   la2_scan_kernel<<<blocks, threads, 0, st>>>(states, decay, init, out, G, BH, H, per, L, reverse);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_scan_kernel launch", e);

@@ -1067,6 +1067,9 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   }
   cfg.gridDim = dim3(p.P * CS);
   cfg.numAttrs = nattr;
+  char kname[48];
+  std::snprintf(kname, sizeof(kname), "la2_tc_kernel<%d,%d,%d,%d>", DK, REV ? 1 : 0, SO ? 1 : 0, CM);
+  LaunchScope log_scope(st, kname, static_cast<int>(cfg.gridDim.x), CS);
   e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, mq1, mk1, mv1, mo1, p);
   if (e != cudaSuccess) return set_cuda_error("la2_tc_kernel launch", e);
   e = cudaGetLastError();

@@ -335,6 +335,23 @@ def workspace_bytes() -> int:
     return int(_lib.load().la2_workspace_bytes())
 
 
+def launch_log(capacity: int) -> None:
+    """Start (capacity > 0) or stop (0) the library's launch log (include/la2.h
+    la2_launch_log): every kernel launch is bracketed by CUDA events on its own stream."""
+    _lib.call("la2_launch_log", int(capacity))
+
+
+def read_launch_log(max_records: int = 65536) -> list:
+    """Logged launches since the last read, in launch order: dicts with the kernel name
+    (as ncu names it), grid, cluster size and event-timed ms. Waits for them."""
+    buf = (_lib.LaunchRecord * max_records)()
+    n = _lib.load().la2_launch_log_read(buf, max_records)
+    if n < 0:
+        _lib.check(n, "la2_launch_log_read")
+    return [{"kernel": r.kernel.decode(), "grid": r.grid, "cluster": r.cluster, "ms": r.ms}
+            for r in buf[:n]]
+
+
 def set_tuning(key: int, value: int) -> None:
     """Process-wide scheduling knob of the tensor-core kernels (include/la2.h
     la2_set_tuning). Outputs do not depend on it."""

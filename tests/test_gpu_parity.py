@@ -842,3 +842,24 @@ def test_acceptance_criterion_4_streaming_on_gpu():
                     port.rel_err(state.kv, ref_state.kv))
         assert state.tokens_absorbed == n
     assert worst <= FP32_TOL, worst
+
+
+def test_launch_log_records_each_kernel():
+    """la2_launch_log brackets every launch with events on its own stream: one forward
+    at d=64 is one la2_tc_kernel<64,0,0,0>; a backward is the dQ F pass plus the dK/dV
+    cluster pair (B*H > SMs: no concurrent side stream at this N)."""
+    from paper_2401_04658_b200 import ops
+    q, k, v, do = gpu(*inputs(2, 16, 32768, 64, 64, torch.bfloat16))
+    ops.launch_log(16)
+    try:
+        ops.la2_forward(q, k, v, 0.9)
+        ops.la2_backward(q, k, v, do, 0.9)
+        recs = ops.read_launch_log()
+    finally:
+        ops.launch_log(0)
+    names = [r["kernel"] for r in recs]
+    assert names == ["la2_tc_kernel<64,0,0,0>", "la2_tc_kernel<64,0,0,0>", "la2_tc_kernel<64,1,0,2>"], recs
+    assert all(r["ms"] > 0 for r in recs) and recs[2]["cluster"] == 2
+    # off: nothing is logged
+    ops.la2_forward(q, k, v, 0.9)
+    assert ops.read_launch_log() == []

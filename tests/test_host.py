@@ -135,13 +135,27 @@ def test_cli_usage_errors_exit_2():
 
 
 def test_bench_roofline_traffic_source():
-    """bench.py's roofline.traffic comes from the committed ncu summary: the file keeps
-    the per-token-head DRAM bytes of the forward F launch, close to the algorithmic 512."""
+    """bench.py's per-launch roofline.traffic comes from the committed ncu summary: DRAM
+    bytes per token-head of each launch of one d=64 step (forward F, dQ F, dK/dV pair),
+    each close to its algorithmic bytes (512, 512, 768)."""
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     sys.path.insert(0, str(root))
     import bench
-    per = bench.load_traffic(1)
-    assert per is not None and 0.9 * 512 <= per <= 1.1 * 512, per
-    assert bench.load_traffic(8 * 16 * 65536) == per * 8 * 16 * 65536
+    per = bench.load_ncu_bytes(64)
+    assert per is not None and set(per) == {"forward", "dq", "dkdv"}, per
+    for role, alg in (("forward", 512), ("dq", 512), ("dkdv", 768)):
+        assert 0.9 * alg <= per[role] <= 1.1 * alg, (role, per)
+
+
+def test_bench_launch_roles():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    recs = [{"kernel": "a", "grid": 1, "cluster": 1, "ms": 1.0}, {"kernel": "b", "grid": 2, "cluster": 2, "ms": 3.0},
+            {"kernel": "a", "grid": 1, "cluster": 1, "ms": 2.0}, {"kernel": "b", "grid": 2, "cluster": 2, "ms": 5.0}]
+    r = bench.launch_roles(recs, ["dq", "dkdv"])
+    assert r["dq"]["ms"] == 1.5 and r["dkdv"]["ms"] == 4.0 and r["dkdv"]["kernel"] == "b"
+    assert bench.launch_roles(recs[:3], ["dq", "dkdv"]) == {}
