@@ -390,7 +390,7 @@ def main():
             soak["window_s"] = soak["ms_per_step"] * n_soak / 1e3
         barrier()
         torch.cuda.synchronize()
-        ms = run_timed(fn, steps)
+        ms = run_timed(fn, steps) if steps > 0 else 0.0
         barrier()
         return max_over_ranks(ms), soak
 

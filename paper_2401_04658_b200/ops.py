@@ -15,6 +15,7 @@ torch stream; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from typing import Optional, Sequence, Union
 
 import torch
@@ -66,7 +67,7 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
         if d.numel() != H:
             raise ValueError(f"decay must have {H} entries (one per head), got {d.numel()}")
         d = d.contiguous()
-        _check_cuda_decay(d)
+        _check_cuda_decay(d, decay)
         return d
     if isinstance(decay, torch.Tensor):
         vals = decay.detach().double().reshape(-1).tolist()
@@ -85,21 +86,29 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
 
 
 _DECAY_CACHE: dict = {}
-_CHECKED: dict = {}  # (data_ptr, numel, device) -> tensor version last validated
+# tensor -> (data_ptr, version) last validated. Keyed by the tensor object (weakly): an
+# address alone is not an identity -- the caching allocator hands a freed decay tensor's
+# memory to the next one.
+# (The map is by id() with a weak reference to confirm identity: tensors cannot be keys of
+# a WeakKeyDictionary, whose lookups compare keys with the tensors' elementwise ==.)
+_CHECKED: dict = {}
 
 
-def _check_cuda_decay(d: torch.Tensor) -> None:
-    """la2_check_decay on a contiguous float32 CUDA decay vector, once per version."""
-    key = (d.data_ptr(), d.numel(), d.device.index)
-    ver = d._version
-    if _CHECKED.get(key) == ver:
+def _check_cuda_decay(d: torch.Tensor, src: Optional[torch.Tensor] = None) -> None:
+    """la2_check_decay on a contiguous float32 CUDA decay vector ``d`` (derived from the
+    caller's tensor ``src``, default ``d``), once per (tensor, version)."""
+    owner = d if src is None else src
+    stamp = (owner.data_ptr(), owner._version)
+    hit = _CHECKED.get(id(owner))
+    if hit is not None and hit[0]() is owner and hit[1] == stamp:
         return
     if torch.cuda.is_current_stream_capturing():
         return  # cannot synchronize inside capture; the kernels poison invalid lam with NaN
     _lib.call("la2_check_decay", d.data_ptr(), d.numel(), _stream(d.device))
-    if len(_CHECKED) >= 1024:
-        _CHECKED.clear()
-    _CHECKED[key] = ver
+    if len(_CHECKED) >= 4096:
+        for key in [k for k, (r, _) in _CHECKED.items() if r() is None]:
+            del _CHECKED[key]
+    _CHECKED[id(owner)] = (weakref.ref(owner), stamp)
 
 
 def _decay(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:

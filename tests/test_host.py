@@ -159,3 +159,29 @@ def test_bench_launch_roles():
     r = bench.launch_roles(recs, ["dq", "dkdv"])
     assert r["dq"]["ms"] == 1.5 and r["dkdv"]["ms"] == 4.0 and r["dkdv"]["kernel"] == "b"
     assert bench.launch_roles(recs[:3], ["dq", "dkdv"]) == {}
+
+
+def test_cuda_decay_check_cache(monkeypatch):
+    """la2_check_decay runs once per (tensor, version): a new tensor at a recycled address,
+    or an in-place change, is checked again (host logic; the C call is stubbed)."""
+    import torch
+    from paper_2401_04658_b200 import ops
+    calls = []
+    monkeypatch.setattr(ops._lib, "call", lambda name, *a: calls.append(name))
+    monkeypatch.setattr(ops, "_stream", lambda dev: 0)
+    monkeypatch.setattr(torch.cuda, "is_current_stream_capturing", lambda: False)
+    t = torch.tensor([0.5, 0.9])
+    ops._check_cuda_decay(t)
+    ops._check_cuda_decay(t)
+    assert calls == ["la2_check_decay"]
+    t.mul_(1.0)  # bumps the version
+    ops._check_cuda_decay(t)
+    assert len(calls) == 2
+    u = torch.tensor([0.5, 0.9])  # another tensor object: checked
+    ops._check_cuda_decay(u)
+    assert len(calls) == 3
+    # a derived vector is cached under the caller's tensor
+    w = torch.tensor([0.5, 0.9], dtype=torch.float64)
+    ops._check_cuda_decay(w.float(), w)
+    ops._check_cuda_decay(w.float(), w)
+    assert len(calls) == 4
