@@ -181,18 +181,20 @@ def c5_phases(q, k, v, do, dec, world, timed_phase):
     B, H, L, D = q.shape
     res = {}
     if world > 1:
+        from paper_2401_04658_b200.sp import cuda_ops
         mode = os.environ.get("LA2_SP_MODE", "allgather")
-        s = ops.chunk_state(k, v, dec)
+        local = cuda_ops("auto")  # the rank's chunk, split into sub-chunks inside the GPU
+        s = local.chunk_state(k, v, dec)
         kv_in = exclusive_scan(s, dec, L, None, reverse=False, mode=mode)
-        t = ops.chunk_dstate(q, do, dec)
+        t = local.chunk_dstate(q, do, dec)
         dkv_in = exclusive_scan(t, dec, L, None, reverse=True, mode=mode)
-        res["fwd_pass_a"] = timed_phase(lambda: ops.chunk_state(k, v, dec))
+        res["sub_chunks_per_rank"] = local.split.get("g", 1)
+        res["fwd_pass_a"] = timed_phase(lambda: local.chunk_state(k, v, dec))
         res["fwd_exchange"] = timed_phase(lambda: exclusive_scan(s, dec, L, None, mode=mode))
-        res["fwd_pass_b"] = timed_phase(lambda: ops.la2_forward(q, k, v, dec, kv_in=kv_in))
-        res["bwd_pass_a"] = timed_phase(lambda: ops.chunk_dstate(q, do, dec))
+        res["fwd_pass_b"] = timed_phase(lambda: local.forward(q, k, v, dec, kv_in))
+        res["bwd_pass_a"] = timed_phase(lambda: local.chunk_dstate(q, do, dec))
         res["bwd_exchange"] = timed_phase(lambda: exclusive_scan(t, dec, L, None, reverse=True, mode=mode))
-        res["bwd_pass_b"] = timed_phase(lambda: ops.la2_backward(q, k, v, do, dec, kv_in=kv_in,
-                                                                 dkv_in=dkv_in))
+        res["bwd_pass_b"] = timed_phase(lambda: local.backward(q, k, v, do, dec, kv_in, dkv_in))
         res["exchange_bytes_per_direction"] = 2 * world * H * D * D * 4
         return res
     g = ops.split_factor(B, H, L, D, D, q.dtype)
@@ -722,6 +724,27 @@ def extra_workload(args, world, rank, local_rank):
             mode = f"sequence parallel x{world} ({os.environ.get('LA2_SP_MODE', 'allgather')}) "
         ms = timed(step, args.steps)
         phases = c5_phases(q.detach(), k.detach(), v.detach(), do, dec, world, timed_phase)
+        if world == 1:
+            # one rank's local work of the 8-GPU run (64K tokens, split into sub-chunks inside
+            # the GPU, carried states from the exchange), without the exchange itself
+            from paper_2401_04658_b200.sp import cuda_ops
+            L8 = N_total // 8
+            q8, k8, v8, do8 = (t.detach()[:, :, :L8].contiguous() for t in (q, k, v, do))
+            local = cuda_ops("auto")
+            kv8 = local.chunk_state(k8, v8, dec)
+            dkv8 = local.chunk_dstate(q8, do8, dec)
+
+            def rank_step():
+                local.chunk_state(k8, v8, dec)
+                local.forward(q8, k8, v8, dec, kv8)
+                local.chunk_dstate(q8, do8, dec)
+                local.backward(q8, k8, v8, do8, dec, kv8, dkv8)
+            ms8 = timed(rank_step, args.steps)
+            phases["sp8_rank_local"] = {"tokens": L8, "sub_chunks": local.split.get("g", 1),
+                                        "ms_fwd_bwd": ms8, "fraction_of_1gpu_step": ms8 / ms,
+                                        "note": "one rank's local passes A+B fwd+bwd of the 8-GPU "
+                                                "sequence-parallel run (exchange excluded)"}
+            del q8, k8, v8, do8
         ff, fb = canonical_flops(N_total, D, D)
         bf, bb = canonical_bytes(N_total, D, D)
         line.update({"metric": "c5 fwd+bwd tokens/s (one 512K sequence)", "value": N_total / (ms / 1e3),

@@ -34,16 +34,86 @@ class LocalOps:
     backward: Callable       # (q, k, v, do, decay, kv_in, dkv_in) -> (dq, dk, dv)
 
 
-def cuda_ops() -> LocalOps:
+def cuda_ops(seq_split="auto") -> LocalOps:
+    """The CUDA kernels as the local compute of one rank, composed with the intra-GPU
+    sequence split (ops.split_factor): with few heads a rank's chunk alone would fill a
+    fraction of the SMs (C5: 16 heads x 2 value slices = 32 CTAs), so each rank cuts its
+    chunk into g sub-chunks and runs the same three phases inside the GPU:
+
+      pass A   sub-chunk states S_j (one chunk_state launch over B*H*g units), combined
+               locally into the rank's chunk state S = lam^(L/g) P_(g-1) + S_(g-1), where
+               P = exclusive prefix of the S_j from zero (la2_state_scan);
+      exchange S across ranks -> KV_in (the caller, exclusive_scan);
+      pass B   sub-chunk carries = exclusive prefix of the S_j seeded with KV_in
+               (la2_state_scan with init), then one forward over the B*H*g units.
+
+    The backward mirrors it with the reverse-sweep states (chunk_dstate, suffix scans).
+    Exact algebra (the fold of pkg/src/tila/kernel.py:111-115 per sub-chunk); returns a
+    fresh object per autograd call (it keeps the sub-chunk states of that call).
+    """
     from . import ops
 
-    return LocalOps(
-        chunk_state=ops.chunk_state,
-        chunk_dstate=ops.chunk_dstate,
-        forward=lambda q, k, v, dec, kv_in: ops.la2_forward(q, k, v, dec, kv_in=kv_in)[0],
-        backward=lambda q, k, v, do, dec, kv_in, dkv_in: ops.la2_backward(
-            q, k, v, do, dec, kv_in=kv_in, dkv_in=dkv_in)[:3],
-    )
+    st: dict = {}
+
+    def factor(B, H, L, d, dv, dtype):
+        g = ops.split_factor(B, H, L, d, dv, dtype) if seq_split == "auto" else int(seq_split)
+        return g if g > 1 and L % g == 0 else 1
+
+    def chunk_state(k, v, dec):
+        B, H, L, d = k.shape
+        dv = v.shape[3]
+        g = st["g"] = factor(B, H, L, d, dv, k.dtype)
+        if g == 1:
+            return ops.chunk_state(k, v, dec)
+        dec_g = dec.repeat_interleave(g)
+        s = ops.chunk_state(ops._chunked(k.contiguous(), g), ops._chunked(v.contiguous(), g), dec_g)
+        s5 = st["s5"] = ops._to_chunk_major(s, B, H, g)
+        pre = ops.state_scan(s5, dec, [L // g] * g)
+        return _decay_pow(dec, torch.tensor(L // g)) * pre[-1] + s5[-1]
+
+    def forward(q, k, v, dec, kv_in):
+        B, H, L, d = q.shape
+        g = st.get("g", 1)
+        if g == 1:
+            return ops.la2_forward(q, k, v, dec, kv_in=kv_in)[0]
+        prefix = ops._from_chunk_major(ops.state_scan(st["s5"], dec, [L // g] * g, init=kv_in), B, H, g)
+        q4, k4, v4 = (ops._chunked(t.contiguous(), g) for t in (q, k, v))
+        o4, _ = ops.la2_forward(q4, k4, v4, dec.repeat_interleave(g), kv_in=prefix)
+        return o4.view(B, H, L, v.shape[3])
+
+    def chunk_dstate(q, do, dec):
+        B, H, L, d = q.shape
+        dv = do.shape[3]
+        g = st["g"] = factor(B, H, L, d, dv, q.dtype)
+        if g == 1:
+            return ops.chunk_dstate(q, do, dec)
+        t = ops.chunk_dstate(ops._chunked(q.contiguous(), g), ops._chunked(do.contiguous(), g),
+                             dec.repeat_interleave(g))
+        t5 = st["t5"] = ops._to_chunk_major(t, B, H, g)
+        suf = ops.state_scan(t5, dec, [L // g] * g, reverse=True)
+        return _decay_pow(dec, torch.tensor(L // g)) * suf[0] + t5[0]
+
+    def backward(q, k, v, do, dec, kv_in, dkv_in):
+        B, H, L, d = q.shape
+        dv = v.shape[3]
+        g = st.get("g", 1)
+        if g == 1:
+            return ops.la2_backward(q, k, v, do, dec, kv_in=kv_in, dkv_in=dkv_in)[:3]
+        if "s5" not in st:  # backward without this object's forward: recompute pass A
+            chunk_state(k, v, dec)
+        lens = [L // g] * g
+        prefix = ops._from_chunk_major(ops.state_scan(st["s5"], dec, lens, init=kv_in), B, H, g)
+        suffix = ops._from_chunk_major(ops.state_scan(st["t5"], dec, lens, init=dkv_in, reverse=True),
+                                       B, H, g)
+        q4, k4, v4, do4 = (ops._chunked(t.contiguous(), g) for t in (q, k, v, do))
+        dq, dk, dvv, _ = ops.la2_backward(q4, k4, v4, do4, dec.repeat_interleave(g), kv_in=prefix,
+                                          dkv_in=suffix)
+        return dq.view(B, H, L, d), dk.view(B, H, L, d), dvv.view(B, H, L, dv)
+
+    ops_ = LocalOps(chunk_state=chunk_state, chunk_dstate=chunk_dstate, forward=forward,
+                    backward=backward)
+    ops_.split = st  # introspection (tests, bench): st["g"] is the sub-chunk count used
+    return ops_
 
 
 def _decay_pow(decay: torch.Tensor, length: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
@@ -148,14 +218,16 @@ class SPLightningAttn2Fn(torch.autograd.Function):
 
 
 def sp_lightning_attn2(q, k, v, decay, group=None, mode: str = "allgather",
-                       local_ops: Optional[LocalOps] = None):
+                       local_ops: Optional[LocalOps] = None, seq_split="auto"):
     """Sequence-parallel lightning_attn2 over ``group``.
 
     Each rank passes its contiguous chunk ``[B, H, N_g, d]`` of one long
     sequence (rank order = sequence order); the result is this rank's chunk of
     the output of the unsharded op. ``decay``: [H] tensor on the local device.
+    ``seq_split``: sub-chunks per rank for the intra-GPU split ("auto" =
+    ops.split_factor of the rank's chunk, 1 = off); see :func:`cuda_ops`.
     """
-    ops_ = local_ops if local_ops is not None else cuda_ops()
+    ops_ = local_ops if local_ops is not None else cuda_ops(seq_split)
     if not isinstance(decay, torch.Tensor):
         decay = torch.tensor(decay, dtype=torch.float32, device=q.device)
     return SPLightningAttn2Fn.apply(q, k, v, decay.float().contiguous(), group, mode, ops_)
