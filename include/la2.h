@@ -22,7 +22,9 @@
  * Element type of q/k/v/o/... is selected by `dtype` (LA2_BF16 or LA2_FP32).
  *
  * Kernel selection is a pure function of (dtype, d, dv):
- *   bf16, d in {64,128}, dv % 64 == 0   -> tcgen05/TMA tensor-core kernel
+ *   bf16, d in {64,128,256}, dv % 64 == 0 -> tcgen05/TMA tensor-core kernel (d = 256:
+ *                                           split-d, two 128-wide passes, the second
+ *                                           adding into o by TMA reduce-add)
  *   otherwise, d <= 256 and dv <= 256   -> SIMT fp32-accumulate kernel
  *   anything else                       -> LA2_ERR_UNSUPPORTED (no fallback)
  *
@@ -81,7 +83,7 @@ LA2_API int la2_forward(const void* q, const void* k, const void* v, const float
  * rows (ldq, ldk, ldv >= N * d / N * dv, multiples of 8), e.g. a [B, H, N, d] slice of
  * a longer sequence, so streaming over chunks of a resident sequence reads the chunks in
  * place (chunked_forward on slices, kernel.py:142-162). o, kv_in, kv_out contiguous.
- * Tensor-core shapes only (bf16, d in {64,128}, dv % 64 == 0); otherwise
+ * Tensor-core shapes only (bf16, d in {64,128,256}, dv % 64 == 0); otherwise
  * LA2_ERR_UNSUPPORTED.
  */
 LA2_API int la2_forward_strided(const void* q, const void* k, const void* v, const float* decay,

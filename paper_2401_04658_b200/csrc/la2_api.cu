@@ -166,11 +166,49 @@ static int join_side(SideStream* side, cudaStream_t st) {
 }
 
 static bool tc_eligible(int dtype, int dk, int dv) {
-  return dtype == LA2_BF16 && (dk == 64 || dk == 128) && dv % 64 == 0 && dv >= 64 && dv <= 256;
+  return dtype == LA2_BF16 && (dk == 64 || dk == 128 || dk == 256) && dv % 64 == 0 && dv >= 64 &&
+         dv <= 256;
+}
+
+// Split-d: an F pass with a 256-wide q/k is the sum of two 128-wide passes over the column
+// halves of q and k, because the scores and the state are linear in the shared dimension:
+//   q_t . k_s = q_t[:128] . k_s[:128] + q_t[128:] . k_s[128:]   (mask and decay are
+//   elementwise, so ((Q K^T) * M) V splits the same way), and the state
+//   sum_s lam^(..) k_s^T v_s splits by rows: rows [0,128) come from the first half only.
+// The first pass stores o, the second adds into it (TMA reduce-add); each pass reads and
+// writes its own 128 rows of kv_in / kv_out. Column halves are read in place (the TMA maps
+// take the row pitch), so no operand is copied.
+static int run_f_split_d(const FArgs& a, cudaStream_t st) {
+  const long long dk = a.dk, dv = a.dv;
+  for (int h = 0; h < 2; ++h) {
+    FArgs b = a;
+    b.dk = 128;
+    b.q = static_cast<const uint16_t*>(a.q) + 128 * h;
+    b.k = static_cast<const uint16_t*>(a.k) + 128 * h;
+    for (int t = 0; t < 2; ++t) b.rp[t] = a.rp[t] ? a.rp[t] : dk;
+    if (a.kv_in != nullptr) {
+      b.kv_in_bhs = a.kv_in_bhs ? a.kv_in_bhs : dk * dv;
+      if (!a.kv_in_T) {
+        b.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : static_cast<int>(dv);
+        b.kv_in = a.kv_in + static_cast<long long>(128) * h * b.kv_in_rs;
+      } else {  // stored [dv][dk]: the pass's rows are the stored columns
+        b.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : static_cast<int>(dk);
+        b.kv_in = a.kv_in + 128 * h;
+      }
+    }
+    if (a.kv_out != nullptr) {
+      b.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : dk * dv;
+      b.kv_out_rs = a.kv_out_rs ? a.kv_out_rs : static_cast<int>(dv);
+      b.kv_out = a.kv_out + static_cast<long long>(128) * h * b.kv_out_rs;
+    }
+    b.accum_o = (h == 1 && a.o != nullptr) ? 1 : a.accum_o;
+    if (int rc = launch_tc(b, st)) return rc;
+  }
+  return 0;
 }
 
 static int run_f(const FArgs& a, cudaStream_t st) {
-  if (tc_eligible(a.dtype, a.dk, a.dv)) return launch_tc(a, st);
+  if (tc_eligible(a.dtype, a.dk, a.dv)) return a.dk == 256 ? run_f_split_d(a, st) : launch_tc(a, st);
   return launch_simt(a, st);
 }
 
@@ -185,7 +223,7 @@ static int check_common(int B, int H, int N, int d, int dv, int dtype, const flo
     char buf[160];
     std::snprintf(buf, sizeof(buf),
                   "unsupported shape d=%d dv=%d for dtype %s (bf16 tensor-core path: d in "
-                  "{64,128}, dv %% 64 == 0; otherwise d, dv <= 256)",
+                  "{64,128,256}, dv %% 64 == 0; otherwise d, dv <= 256)",
                   d, dv, dtype == LA2_BF16 ? "bf16" : "fp32");
     return set_error(LA2_ERR_UNSUPPORTED, buf);
   }
@@ -255,7 +293,7 @@ int la2_forward_strided(const void* q, const void* k, const void* v, const float
   if (!q || !k || !v || !o) return set_error(LA2_ERR_VALUE, "null tensor pointer");
   if (!tc_eligible(dtype, d, dv))
     return set_error(LA2_ERR_UNSUPPORTED,
-                     "strided inputs need the tensor-core path (bf16, d in {64,128}, dv % 64 == 0)");
+                     "strided inputs need the tensor-core path (bf16, d in {64,128,256}, dv % 64 == 0)");
   const long long need[3] = {1LL * N * d, 1LL * N * d, 1LL * N * dv};
   const long long ld[3] = {ldq, ldk, ldv};
   for (int t = 0; t < 3; ++t)
@@ -304,7 +342,7 @@ int la2_backward_strided(const void* q, const void* k, const void* v, const void
   g_err[0] = 0;
   if (!tc_eligible(dtype, d, dvd))
     return set_error(LA2_ERR_UNSUPPORTED,
-                     "strided inputs need the tensor-core path (bf16, d in {64,128}, dv % 64 == 0)");
+                     "strided inputs need the tensor-core path (bf16, d in {64,128,256}, dv % 64 == 0)");
   const long long ld[4] = {ldq, ldk, ldv, lddo};
   const long long need[4] = {1LL * N * d, 1LL * N * d, 1LL * N * dvd, 1LL * N * dvd};
   for (int t = 0; t < 4; ++t)

@@ -36,6 +36,14 @@ struct FArgs {
   // elements between consecutive (b, h) rows of q, k, v, o (0 = contiguous N * cols);
   // tensor-core path only (the TMA maps carry the stride)
   long long ld[4] = {0, 0, 0, 0};
+  // elements between consecutive tokens of q, k, v, o (0 = the operand's width): column
+  // slices of a wider tensor (split-d). Tensor-core path only.
+  long long rp[4] = {0, 0, 0, 0};
+  // state addressing (0 = contiguous [B,H,dk,dv]): element (r, c) of the pass's state for
+  // head bh is at bh * bhs + r * rs + c (kv_in_T: bh * bhs + c * rs + r)
+  long long kv_in_bhs = 0, kv_out_bhs = 0;
+  int kv_in_rs = 0, kv_out_rs = 0;
+  int accum_o = 0;  // add the output into o (TMA reduce-add) instead of storing it
 };
 
 // Kernel-side parameter block (passed by value).
@@ -53,6 +61,10 @@ struct FParams {
   int units, P, nsl;
   float* ws;   // [P * cluster][dk][64] fp32 state handoff between neighbouring ranges
   int* flags;  // [P * cluster] handoff flags (0 = empty), reset by their reader
+  // state addressing (see FArgs); resolved to the contiguous defaults by the launcher
+  long long kv_in_bhs, kv_out_bhs;
+  int kv_in_rs, kv_out_rs;
+  int accum;  // output epilogue: TMA reduce-add into o
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);
@@ -63,7 +75,8 @@ int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 // TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle;
 // head_stride = elements between (b, h) rows (0: N * cols).
 int tma_encoder_ready();
-int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows, long long head_stride = 0);
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows, long long head_stride = 0,
+                   long long row_pitch = 0);
 int launch_simt(const FArgs& a, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);

@@ -657,7 +657,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           named_bar_sync(1 + q4, 64);
           if (storer) {
-            if (p.hint & 4)
+            if (p.accum)
+              tma_reduce_add_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
+            else if (p.hint & 4)
               tma_store_3d_hint(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh,
                                 l2_policy_evict_first());
             else
@@ -686,20 +688,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
       if (pos == 0) {
         if (p.kv_in != nullptr && has_kv) {
-          const size_t sbase = static_cast<size_t>(bh) * DK * dvt;
+          const size_t sbase = static_cast<size_t>(bh) * p.kv_in_bhs;
           const int c0 = slice * DVS;
           if (!kv_in_T) {
-            const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * dvt + c0;
+            const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * p.kv_in_rs + c0;
 #pragma unroll
             for (int j = 0; j < DVS; j += 4) {
               float4 w = *reinterpret_cast<const float4*>(src + j);
               kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
             }
           } else {
-            // state stored transposed: [dv_total][DK]
+            // state stored transposed: element (r, c) at c * rs + r
 #pragma unroll
             for (int j = 0; j < DVS; ++j)
-              kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * DK + kvrow];
+              kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * p.kv_in_rs + kvrow];
           }
         }
       } else {
@@ -722,8 +724,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     auto store_state = [&](int bh, int slice, int pos) {
       if (pos == nblk - 1) {
         if (kv_out != nullptr && has_kv) {
-          float* dst = kv_out + static_cast<size_t>(bh) * DK * dvt + static_cast<size_t>(kvrow) * dvt +
-                       slice * DVS;
+          float* dst = kv_out + static_cast<size_t>(bh) * p.kv_out_bhs +
+                       static_cast<size_t>(kvrow) * p.kv_out_rs + slice * DVS;
 #pragma unroll
           for (int j = 0; j < DVS; j += 4)
             *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
@@ -879,38 +881,40 @@ int tma_encoder_ready() { return get_encode(); }
 // Tensor maps depend only on (address, shape, box), so they are cached per host thread
 // (a map for the same address and shape is valid whatever tensor now lives there).
 static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT,
-                     long long head_stride = 0) {
+                     long long head_stride = 0, long long row_pitch = 0) {
   struct Entry {
     const void* ptr;
     int cols, N, BH, box;
-    long long ld;
+    long long ld, rp;
     CUtensorMap map;
   };
   static thread_local Entry cache[32];
   static thread_local int next = 0;
   for (const Entry& e : cache) {
     if (e.ptr == ptr && e.cols == cols && e.N == N && e.BH == BH && e.box == box_rows &&
-        e.ld == head_stride && ptr) {
+        e.ld == head_stride && e.rp == row_pitch && ptr) {
       *m = e.map;
       return 0;
     }
   }
-  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows, head_stride);
+  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows, head_stride, row_pitch);
   if (rc == 0) {
     Entry& e = cache[next];
     next = (next + 1) & 31;
     e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.ld = head_stride;
+    e.rp = row_pitch;
     e.map = *m;
   }
   return rc;
 }
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows,
-                   long long head_stride) {
+                   long long head_stride, long long row_pitch) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
                         static_cast<cuuint64_t>(BH)};
+  const cuuint64_t rp = row_pitch > 0 ? static_cast<cuuint64_t>(row_pitch) : static_cast<cuuint64_t>(cols);
   const cuuint64_t ld = head_stride > 0 ? static_cast<cuuint64_t>(head_stride)
-                                        : static_cast<cuuint64_t>(cols) * static_cast<cuuint64_t>(N);
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, ld * 2};
+                                        : rp * static_cast<cuuint64_t>(N);
+  cuuint64_t strides[2] = {rp * 2, ld * 2};
   cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
@@ -988,7 +992,8 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     if (SO && t != 1 && t != 2) continue;
     if (CM != 3 && (t == 5 || t == 6)) continue;
     const long long ld = (t < 4) ? a.ld[t] : (a1 ? a1->ld[t - 4] : a.ld[t - 4]);
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT, ld);
+    const long long rp = (t < 4) ? a.rp[t] : (a1 ? a1->rp[t - 4] : a.rp[t - 4]);
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT, ld, rp);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),
@@ -1007,6 +1012,11 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
+  p.kv_in_bhs = a.kv_in_bhs ? a.kv_in_bhs : static_cast<long long>(DK) * a.dv;
+  p.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : (a.kv_in_T ? DK : a.dv);
+  p.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : static_cast<long long>(DK) * a.dv;
+  p.kv_out_rs = a.kv_out_rs ? a.kv_out_rs : a.dv;
+  p.accum = a.accum_o;
   p.pf = prefetch_blocks();
   p.hint = l2_hints();
   // persistent schedule: units = independent recurrences (a cluster's pair counts once)
