@@ -314,7 +314,9 @@ def main():
     if args.workload != "c2" and args.impl == "ours":
         return extra_workload(args, world, rank, local_rank)
     B, H, N, D = args.batch, args.heads, args.seq_len, args.dim
-    config = {"workload": "TransNormerLLM-400M attention (BASELINE configs[1]) fwd+bwd",
+    config = {"workload": "TransNormerLLM-400M attention (BASELINE configs[1]) fwd+bwd" if D == 64 else
+              f"BASELINE configs[1] shape at head dim {D} (split-d variant)" if D == 256 else
+              f"BASELINE configs[1] shape at head dim {D}",
               "batch_per_gpu": B, "global_batch": B * world, "heads": H, "head_dim": D,
               "seq_len": N, "decay": "alibi-style exp(-2^(-8(h+1)/H))",
               "parallelism": f"bxh-shard x{world}" if world > 1 else "single",
@@ -407,7 +409,7 @@ def main():
     # ---------------- per-launch times (launch log: events on the launching stream)
     # in the sustained regime, like the headline
     time_steps(lambda: step(q, k, v, do), 0, 0, soak_s=args.soak_s)
-    ops.launch_log(4 * max(3, args.steps) + 8)
+    ops.launch_log(16 * max(3, args.steps) + 8)
     for _ in range(max(3, args.steps)):
         la2.la2_forward(q, k, v, decay)
     fwd_log = ops.read_launch_log()
@@ -417,10 +419,18 @@ def main():
     ops.launch_log(0)
     n_f = max(3, args.steps)
     per_call_f, per_call_b = len(fwd_log) // n_f, len(bwd_log) // n_f
-    roles = launch_roles(fwd_log, ["forward"] * per_call_f if per_call_f == 1 else
-                         [f"forward{i}" for i in range(per_call_f)])
-    roles.update(launch_roles(bwd_log, ["dq", "dkdv"] if per_call_b == 2 else
-                              [f"backward{i}" for i in range(per_call_b)]))
+    if per_call_f == 1 and per_call_b == 2:  # d = 64: forward F | dQ F, dK/dV pair
+        roles = launch_roles(fwd_log, ["forward"])
+        roles.update(launch_roles(bwd_log, ["dq", "dkdv"]))
+    else:  # other shapes (split-d, separate dK / dV passes): one entry per direction
+        roles = {}
+        for name, log, per in (("forward", fwd_log, per_call_f), ("backward", bwd_log, per_call_b)):
+            r = launch_roles(log, [f"{name}{i}" for i in range(per)])
+            if r:
+                roles[name] = {"kernel": " + ".join(sorted({x["kernel"] for x in r.values()})),
+                               "grid": max(x["grid"] for x in r.values()),
+                               "cluster": max(x["cluster"] for x in r.values()),
+                               "ms": sum(x["ms"] for x in r.values()), "launches_per_call": per}
     launches_per_step = per_call_f + per_call_b
 
     # ---------------- headline: sustained (soak, then exactly K timed steps)
@@ -436,17 +446,21 @@ def main():
     e = 2
     alg = {"forward": B * H * N * e * (2 * D + 2 * D),   # read q, k, v; write o
            "dq": B * H * N * e * (2 * D + 2 * D),        # read dO, V, K; write dQ
-           "dkdv": B * H * N * e * (3 * D + 3 * D)}      # read K, Q, dO, V; write dK, dV
+           "dkdv": B * H * N * e * (3 * D + 3 * D),      # read K, Q, dO, V; write dK, dV
+           "backward": bb * B * H}                        # SURVEY 8d compulsory backward bytes
     ncu_bytes = load_ncu_bytes(D)
     launches = []
     for role, r in roles.items():
         a_bytes = alg.get(role)
         ent = {"role": role, "kernel": r["kernel"], "grid": r["grid"], "cluster": r["cluster"],
                "launch_ms": r["ms"]}
+        if "launches_per_call" in r:
+            ent["launches_per_call"] = r["launches_per_call"]
         if a_bytes:
             ach = a_bytes / (r["ms"] / 1e3) / 1e9
             ent.update({"algorithmic_bytes": a_bytes, "achieved_gbs": ach, "frac": ach / hbm_peak,
-                        "traffic": (ncu_bytes[role] * B * H * N) if ncu_bytes else None})
+                        "traffic": (ncu_bytes[role] * B * H * N) if ncu_bytes and role in ncu_bytes
+                        else None})
         launches.append(ent)
     sum_launch = sum(x["launch_ms"] for x in launches) or 1.0
     for x in launches:
@@ -555,7 +569,7 @@ def main():
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC if D == 64 else METRIC.replace("d=64", f"d={D}"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": config, "tflops": tflops,
