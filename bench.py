@@ -269,8 +269,9 @@ def launch_roles(recs, roles):
 
 
 def load_ncu_bytes(d: int):
-    """DRAM bytes per (token, head) of each launch of one fwd+bwd step (forward F, dQ F,
-    dK/dV pair) from the committed ncu --set full capture (profiles/ncu_summary.json)."""
+    """DRAM bytes per (token, head) of each launch of one fwd+bwd step (d = 64: forward F
+    with stored states, dQ/dK/dV triple; or forward F, dQ F, dK/dV pair) from the committed
+    ncu --set full capture (profiles/ncu_summary.json)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
@@ -279,10 +280,10 @@ def load_ncu_bytes(d: int):
         key = f"full_d{d}"
         th = j["token_heads"][key]
         ls = j["launches"][key]
-        if len(ls) != 3:
+        roles = {2: ("forward", "backward"), 3: ("forward", "dq", "dkdv")}.get(len(ls))
+        if roles is None:
             return None
-        return {role: (x["dram_read_bytes"] + x["dram_write_bytes"]) / th
-                for role, x in zip(("forward", "dq", "dkdv"), ls)}
+        return {role: (x["dram_read_bytes"] + x["dram_write_bytes"]) / th for role, x in zip(roles, ls)}
     except Exception:
         return None
 
@@ -365,9 +366,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # what the autograd entry point runs at a shape (ops.LightningAttn2Fn's policy)
+    use_stored = lambda n: ops.STORED_STATES and D == 64 and n >= ops.STORED_STATES_MIN_N  # noqa: E731
+    stored = use_stored(N)
+
     def step(q, k, v, do):
-        la2.la2_forward(q, k, v, decay)
-        la2.la2_backward(q, k, v, do, decay)
+        # the device work of one lightning_attn2 training step (LightningAttn2Fn): d = 64
+        # stores the per-block states and runs the dQ/dK/dV triple; otherwise replay
+        if use_stored(q.shape[2]):
+            _, _, blocks = ops.la2_forward_states(q, k, v, decay)
+            ops.la2_backward_states(q, k, v, do, decay, blocks)
+        else:
+            la2.la2_forward(q, k, v, decay)
+            la2.la2_backward(q, k, v, do, decay)
 
     def run_timed(fn, steps):
         """Device time per call of `steps` back-to-back calls (events on torch's current
@@ -410,16 +421,27 @@ def main():
     # in the sustained regime, like the headline
     time_steps(lambda: step(q, k, v, do), 0, 0, soak_s=args.soak_s)
     ops.launch_log(16 * max(3, args.steps) + 8)
+    blocks = None
     for _ in range(max(3, args.steps)):
-        la2.la2_forward(q, k, v, decay)
+        if stored:
+            _, _, blocks = ops.la2_forward_states(q, k, v, decay)
+        else:
+            la2.la2_forward(q, k, v, decay)
     fwd_log = ops.read_launch_log()
     for _ in range(max(3, args.steps)):
-        la2.la2_backward(q, k, v, do, decay)
+        if stored:
+            ops.la2_backward_states(q, k, v, do, decay, blocks)
+        else:
+            la2.la2_backward(q, k, v, do, decay)
     bwd_log = ops.read_launch_log()
     ops.launch_log(0)
+    del blocks
     n_f = max(3, args.steps)
     per_call_f, per_call_b = len(fwd_log) // n_f, len(bwd_log) // n_f
-    if per_call_f == 1 and per_call_b == 2:  # d = 64: forward F | dQ F, dK/dV pair
+    if per_call_f == 1 and per_call_b == 1:  # d = 64 stored states: forward F | dQ/dK/dV triple
+        roles = launch_roles(fwd_log, ["forward"])
+        roles.update(launch_roles(bwd_log, ["backward"]))
+    elif per_call_f == 1 and per_call_b == 2:  # d = 64 replay: forward F | dQ F, dK/dV pair
         roles = launch_roles(fwd_log, ["forward"])
         roles.update(launch_roles(bwd_log, ["dq", "dkdv"]))
     else:  # other shapes (split-d, separate dK / dV passes): one entry per direction

@@ -118,6 +118,27 @@ LA2_API int la2_backward_strided(const void* q, const void* k, const void* v, co
                                  long long ldk, long long ldv, long long lddo, void* stream);
 
 /*
+ * Forward that also stores the per-block states, and the backward that uses them
+ * (bf16, d = dv = 64; otherwise LA2_ERR_UNSUPPORTED).
+ * kv_blocks: [B, H, ceil(N/128), d, dv] bf16, la2_state_blocks_bytes() bytes: entry
+ * [b, h, i] is the bf16 state KV_{i-1} the forward's block i read (128-token blocks;
+ * i = 0: kv_in or 0) -- the KV the reference's sweep 1 replays (kernel.py:184-204).
+ * la2_backward_states then computes dQ block by block from the stored states instead
+ * of replaying the recurrence, inside the same 3-CTA cluster as the dK / dV reverse
+ * scans (kernel.py:207-231), so K, Q, dO and V are read once. Results equal
+ * la2_backward's up to the rounding of the replayed state (both bf16).
+ * dkv_in / dkv_out as in la2_backward; the forward's kv_in is in kv_blocks already.
+ */
+LA2_API long long la2_state_blocks_bytes(int B, int H, int N, int d, int dv);
+LA2_API int la2_forward_states(const void* q, const void* k, const void* v, const float* decay,
+                               void* o, const float* kv_in, float* kv_out, void* kv_blocks, int B,
+                               int H, int N, int d, int dv, int dtype, void* stream);
+LA2_API int la2_backward_states(const void* q, const void* k, const void* v, const void* dout,
+                                const float* decay, const void* kv_blocks, void* dq, void* dk,
+                                void* dv, const float* dkv_in, float* dkv_out, int B, int H, int N,
+                                int d, int dv_dim, int dtype, void* stream);
+
+/*
  * Chunk-local forward state only (no output): S = sum_s lam^(N-1-s) k_s^T v_s.
  * Equals the KvState.kv returned by tila.chunked_forward from a fresh state
  * (pkg/src/tila/kernel.py:142-162). Sequence-parallel pass A.

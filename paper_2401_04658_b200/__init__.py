@@ -21,7 +21,9 @@ from .ops import (
     decay_tensor,
     decode_step,
     la2_backward,
+    la2_backward_states,
     la2_forward,
+    la2_forward_states,
     lightning_attn2,
     set_tuning,
     split_backward,
@@ -42,7 +44,9 @@ __all__ = [
     "decode_step",
     "exclusive_scan",
     "la2_backward",
+    "la2_backward_states",
     "la2_forward",
+    "la2_forward_states",
     "lightning_attn2",
     "set_tuning",
     "sp_lightning_attn2",

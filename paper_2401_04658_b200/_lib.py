@@ -46,12 +46,17 @@ SIGNATURES: dict[str, list] = {
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_check_decay": [_vp, _i, _vp],
+    "la2_state_blocks_bytes": [_i, _i, _i, _i, _i],
+    "la2_forward_states": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "la2_backward_states": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
+                            _vp],
     "la2_launch_log": [_i],
     "la2_launch_log_read": [ctypes.POINTER(LaunchRecord), _i],
     "la2_set_tuning": [_i, _i],
     "la2_workspace_bytes": [],
 }
 _RESTYPES = {"la2_last_error": ctypes.c_char_p, "la2_workspace_bytes": ctypes.c_longlong,
+             "la2_state_blocks_bytes": ctypes.c_longlong,
              "la2_dev_last_error": ctypes.c_char_p}
 _DEV_ONLY = {"la2_set_tuning"}
 

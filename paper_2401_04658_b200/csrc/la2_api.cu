@@ -438,6 +438,48 @@ static int backward_reverse(const void* q, const void* k, const void* v, const v
   return run_f(av, st);
 }
 
+long long la2_state_blocks_bytes(int B, int H, int N, int d, int dv) {
+  if (B < 1 || H < 1 || N < 1 || d < 1 || dv < 1) return 0;
+  return 2LL * B * H * ((N + 127) / 128) * d * dv;
+}
+
+static bool states_eligible(int dtype, int d, int dv) { return dtype == LA2_BF16 && d == 64 && dv == 64; }
+
+int la2_forward_states(const void* q, const void* k, const void* v, const float* decay, void* o,
+                       const float* kv_in, float* kv_out, void* kv_blocks, int B, int H, int N,
+                       int d, int dv, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (!states_eligible(dtype, d, dv))
+    return set_error(LA2_ERR_UNSUPPORTED, "stored per-block states need bf16 with d = dv = 64");
+  if (!q || !k || !v || !o || !kv_blocks) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  FArgs a{q, k, v, o, decay, kv_in, 0, kv_out, B, H, N, d, dv, dtype, 0};
+  a.kv_blocks = kv_blocks;
+  return launch_tc(a, static_cast<cudaStream_t>(stream));
+}
+
+int la2_backward_states(const void* q, const void* k, const void* v, const void* dout,
+                        const float* decay, const void* kv_blocks, void* dq, void* dk, void* dv,
+                        const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dvd,
+                        int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dvd, dtype, decay)) return rc;
+  if (!states_eligible(dtype, d, dvd))
+    return set_error(LA2_ERR_UNSUPPORTED, "stored per-block states need bf16 with d = dv = 64");
+  if (!q || !k || !v || !dout || !dq || !dk || !dv || !kv_blocks)
+    return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  // dV = F_rev(K, Q, dO) (state dKV), dK = F_rev(V, dO, Q) (state dKV^T): the reverse
+  // sweep of kernel.py:207-231; dQ = F(dO, V, K) from the stored KV_{i-1}: sweep 1
+  // (kernel.py:184-204) without replaying the recurrence.
+  FArgs av{k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, dtype, 1};
+  FArgs ak{v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, dtype, 1};
+  FArgs aq{dout, v, k, dq, decay, nullptr, 0, nullptr, B, H, N, dvd, d, dtype, 0};
+  aq.kv_blocks = const_cast<void*>(kv_blocks);
+  return launch_tc_triple(av, ak, aq, static_cast<cudaStream_t>(stream));
+}
+
 int la2_chunk_state(const void* k, const void* v, const float* decay, float* s_out, int B, int H,
                     int N, int d, int dv, int dtype, void* stream) {
   g_err[0] = 0;

@@ -44,6 +44,9 @@ struct FArgs {
   long long kv_in_bhs = 0, kv_out_bhs = 0;
   int kv_in_rs = 0, kv_out_rs = 0;
   int accum_o = 0;  // add the output into o (TMA reduce-add) instead of storing it
+  // per-block bf16 states [B*H][ceil(N/128)][dk][dv] (d = dv = 64): written by a forward
+  // (store), read by the backward triple's dQ CTA
+  void* kv_blocks = nullptr;
 };
 
 // Kernel-side parameter block (passed by value).
@@ -65,11 +68,15 @@ struct FParams {
   long long kv_in_bhs, kv_out_bhs;
   int kv_in_rs, kv_out_rs;
   int accum;  // output epilogue: TMA reduce-add into o
+  int store_states;  // forward (d = 64): write the per-block bf16 states through tm_v1
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);
 // dV and dK reverse scans as one 2-CTA cluster per head (shared Q / dO tiles).
 int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st);
+// d = dv = 64 with stored per-block states (adq.kv_blocks): dV, dK and a stateless dQ pass
+// as one 3-CTA cluster per head.
+int launch_tc_triple(const FArgs& adv, const FArgs& adk, const FArgs& adq, cudaStream_t st);
 // d = dv = 128: dV and dK reverse scans as one 4-CTA cluster per unit (two value-slice pairs).
 int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 // TMA tensor map of a [BH][N][cols] bf16 tensor, box (64 cols, box_rows, 1), 128B swizzle;

@@ -59,21 +59,24 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #define LA2_SO_NS 4
 #endif
 
-template <int DK, bool SO>
+template <int DK, bool SO, bool TRI = false>
 struct TcLayout {
   // Q/K/V stages; state-only passes stage only K and V (32 / 48 KB), so they get a deeper ring
   static constexpr int NS = SO ? LA2_SO_NS : ((DK == 64) ? 3 : 2);
   static constexpr int KTS = 2;                   // V~ buffers (scaled values)
-  static constexpr int OS = (DK == 64 && !SO) ? 2 : 1;  // O staging buffers
+  // O staging buffers (the backward triple spends the second one on its state tiles)
+  static constexpr int OS = (DK == 64 && !SO && !TRI) ? 2 : 1;
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
   static constexpr int K_BYTES = BT * DK * 2;
   static constexpr int V_BYTES = BT * DVS * 2;
+  static constexpr int S_BYTES = TRI ? DK * DVS * 2 : 0;  // triple: stored bf16 state per stage
   static constexpr int KV_BYTES = SO ? 0 : DK * DVS * 2;
   static constexpr int O_BYTES = SO ? 0 : BT * DVS * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
-  static constexpr int OFF_KT = OFF_V + NS * V_BYTES;
+  static constexpr int OFF_S = OFF_V + NS * V_BYTES;
+  static constexpr int OFF_KT = OFF_S + NS * S_BYTES;
   static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
   static constexpr int OFF_O = OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
@@ -114,6 +117,13 @@ struct TcLayout {
 //   CM = 2  backward pair: rank 0 runs F_rev(K, Q, dO) -> dV, rank 1 runs
 //           F_rev(V, dO, Q) -> dK; the Q and dO tiles are shared (rank 0 loads Q,
 //           rank 1 loads dO) and play swapped k/v roles in the two CTAs
+//   CM = 4  backward triple (d = dv = 64, with the per-block states the forward stored):
+//           ranks 0-1 as CM 2, rank 2 computes dQ = F(dO, V, K) block by block from the
+//           stored state KV_{i-1} (no recurrence), walking the same blocks in lockstep: dO
+//           is multicast to all three, K from rank 0 to ranks 0 and 2, rank 2 loads V
+//           itself (an L2 hit: rank 1 loads the same tile at the same time) and the state
+//           tile. The backward then reads K, Q, dO, V once instead of also re-reading dO,
+//           V, K for a separate dQ scan.
 template <int DK, bool REV, bool SO, int CM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     la2_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -121,10 +131,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   const __grid_constant__ CUtensorMap tm_q1, const __grid_constant__ CUtensorMap tm_k1,
                   const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_o1,
                   const FParams p) {
-  using L = TcLayout<DK, SO>;
+  using L = TcLayout<DK, SO, CM == 4>;
   constexpr bool CL = (CM != 0);
-  constexpr int CS = (CM == 3) ? 4 : (CL ? 2 : 1);  // CTAs per cluster
+  constexpr int CS = (CM == 3) ? 4 : ((CM == 4) ? 3 : (CL ? 2 : 1));  // CTAs per cluster
   static_assert(CM != 2 || (DK == 64 && REV && !SO), "backward pair needs d = dv = 64");
+  static_assert(CM != 4 || (DK == 64 && REV && !SO), "backward triple needs d = dv = 64");
   static_assert(CM != 3 || (DK == 128 && REV && !SO), "backward quad needs d = dv = 128");
   static_assert(!(SO && CM >= 2), "state-only passes run alone or as value-slice pairs");
   constexpr int NS = L::NS, KTS = L::KTS, OS = L::OS;
@@ -141,16 +152,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // CM 3: ranks 0-1 run one pass (value-slice pair), ranks 2-3 the sibling pass
   const int pair = (CM == 3) ? static_cast<int>(crank >> 1) : 0;
   const uint32_t prank = (CM == 3) ? (crank & 1) : crank;    // rank inside the pair
-  const uint16_t mcmask = static_cast<uint16_t>(0x3u << (2 * pair));  // this pair's CTAs
-  const bool sib = ((CM == 2) && (crank == 1)) || ((CM == 3) && pair == 1);  // sibling pass
-  const CUtensorMap* mq = sib ? &tm_q1 : &tm_q;
-  const CUtensorMap* mo = sib ? &tm_o1 : &tm_o;
+  // this pair's CTAs (the triple: all three)
+  const uint16_t mcmask = (CM == 4) ? uint16_t(0x7) : static_cast<uint16_t>(0x3u << (2 * pair));
+  const bool dqr = (CM == 4) && (crank == 2);  // the triple's stateless dQ CTA
+  const bool rrev = REV && !dqr;               // scan direction of this CTA's masks / factors
+  const bool sib = ((CM == 2 || CM == 4) && (crank == 1)) || ((CM == 3) && pair == 1);  // sibling pass
+  const CUtensorMap* mq = (sib || dqr) ? &tm_q1 : &tm_q;  // dqr: its own copy of V (tm_q1)
+  const CUtensorMap* mo = dqr ? &tm_k1 : (sib ? &tm_o1 : &tm_o);  // dqr: dQ through tm_k1
   const CUtensorMap* mk = (CM == 3 && sib) ? &tm_k1 : &tm_k;
   const CUtensorMap* mv = (CM == 3 && sib) ? &tm_v1 : &tm_v;
-  const int offk = (CM == 2 && sib) ? L::OFF_V : L::OFF_K;  // this CTA's k tile region
-  const int offv = (CM == 2 && sib) ? L::OFF_K : L::OFF_V;  // this CTA's v tile region
+  // smem regions of this CTA's q / k / v roles. Pair and triple: Q at OFF_K, dO at OFF_V,
+  // the CTA's own q (K | V) at OFF_Q; the dQ CTA: q = dO (OFF_V), k = V (own load, OFF_K),
+  // v = K (multicast by rank 0, OFF_Q), plus the stored state tile at OFF_S
+  const int offq = dqr ? L::OFF_V : L::OFF_Q;
+  const int offk = dqr ? L::OFF_K : (((CM == 2 || CM == 4) && sib) ? L::OFF_V : L::OFF_K);
+  const int offv = dqr ? L::OFF_Q : (((CM == 2 || CM == 4) && sib) ? L::OFF_K : L::OFF_V);
   const int kv_in_T = sib ? 1 : p.kv_in_T;          // the dK pass carries dKV^T
-  float* const kv_out = sib ? nullptr : p.kv_out;
+  float* const kv_out = (sib || dqr) ? nullptr : p.kv_out;
   const int N = p.N;
   const int nblk = (N + BT - 1) / BT;
   const int cid = blockIdx.x / CS;                  // this CTA's (cluster's) work range
@@ -170,7 +188,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[L::B_FULL + s], 1);
       // X after PV, Y after Oe (x2 in a cluster: the stage is shared)
-      mbar_init(&bars[L::B_EMPTY + s], (SO ? 1 : 2) * (CL ? 2 : 1));
+      mbar_init(&bars[L::B_EMPTY + s], (SO ? 1 : 2) * (CM == 4 ? 3 : (CL ? 2 : 1)));
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[L::B_SFULL + b], 1);
@@ -196,6 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch_desc(mk);
     tma_prefetch_desc(mv);
     if (!SO) tma_prefetch_desc(mo);
+    if (dqr) tma_prefetch_desc(&tm_v1);
   }
   if (warp == 1) tmem_alloc(tmem_slot, L::TMEM_COLS);
   if (threadIdx.x == 0) {
@@ -285,7 +304,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      ((w.pos == nblk - 1 || g == sch.npre - 1) ? REC_SEG_END : 0);
           recs[g & 7] = rc;
         }
-        mbar_arrive_expect_tx(&bars[L::B_FULL + s], L::STAGE_TX);
+        mbar_arrive_expect_tx(&bars[L::B_FULL + s], dqr ? L::STAGE_TX + L::S_BYTES : L::STAGE_TX);
         const int row = blk * BT;
         uint64_t* fb = &bars[L::B_FULL + s];
         uint8_t* dq = smem + L::OFF_Q + s * L::Q_BYTES;
@@ -308,10 +327,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
           tma_load_3d(dv, mv, fb, slice * DVS, row, bh);
-        } else {
+        } else if (CM == 2) {
           tma_load_3d(dq, mq, fb, 0, row, bh);  // own q: K (rank 0) or V (rank 1)
           if (crank == 0) tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K
           else tma_load_3d_mc(dv, &tm_v, fb, 0, row, bh, 0x3);             // dO -> region V
+        } else {  // CM 4
+          if (crank == 0) {
+            tma_load_3d_mc(dq, mq, fb, 0, row, bh, 0x5);    // K -> OFF_Q of ranks 0 and 2
+            tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K of ranks 0, 1
+          } else if (crank == 1) {
+            tma_load_3d(dq, mq, fb, 0, row, bh);             // V (own q of the dK pass)
+            tma_load_3d_mc(dv, &tm_v, fb, 0, row, bh, 0x7);  // dO -> region V of all three
+          } else {
+            tma_load_3d(dk, mq, fb, 0, row, bh);             // V (the dQ pass's k)
+            tma_load_3d(smem + L::OFF_S + s * L::S_BYTES, &tm_v1, fb, 0, blk * DK, bh);  // KV_{blk-1}
+          }
         }
       }
       if (CL) {
@@ -329,7 +359,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool leader = (lane == 0);
     const uint32_t tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
     // descriptor bases (start address is in 16-byte units in the low bits)
-    const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
+    constexpr uint32_t ID_OS = idesc_bf16(128, DVS, 0, 0);  // dO (K-major) x stored KV (K-major)
+    const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + offq), 16, 1024);
+    const uint64_t dS0 = sdesc_sw128(smem_u32(smem + L::OFF_S), 16, 1024);
     const uint64_t dK0 = sdesc_sw128(smem_u32(smem + offk), 16, 1024);
     const uint64_t dV0 = sdesc_sw128(smem_u32(smem + offv), REGION, 1024);
     auto commit_empty = [&](int s) {
@@ -447,6 +479,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ---- Y: state chain  dKV_i = K~_i^T V_i (early) ; Oe_i = Q_i KV_{i-1}
       for (int i = 0; i < T; ++i) {
         const int s = i % NS, kt = i % KTS, db = i & 1;
+        if (dqr) {
+          // the triple's dQ CTA: no recurrence; Oe_i = dO_i (KV_{i-1})^T from the stored state
+          mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
+          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          tc_fence_after();
+          if (leader) {
+            const uint64_t q = adv(dQ0, s * L::Q_BYTES), st = adv(dS0, s * L::S_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < DVS / 16; ++kk)
+              umma_bf16_ss(tOE, adv(q, (kk & 3) * 32), adv(st, (kk & 3) * 32), ID_OS, kk > 0);
+            umma_commit(&bars[L::B_OEFULL + db]);
+            commit_empty(s);
+          }
+          __syncwarp();
+          continue;
+        }
         mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
         if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
         mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
@@ -502,8 +550,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       float G[16], F[4], MX[2][16];
       const int dch = row >> 4, tt = row & 15;
       const int hm = q4 - 2 * half;  // the straddling half (0/1) or none
-      const int kind0 = (2 * half == q4) ? 2 : ((REV ? 2 * half > q4 : 2 * half < q4) ? 1 : 0);
-      const int kind1 = (2 * half + 1 == q4) ? 2 : ((REV ? 2 * half + 1 > q4 : 2 * half + 1 < q4) ? 1 : 0);
+      const int kind0 = (2 * half == q4) ? 2 : ((rrev ? 2 * half > q4 : 2 * half < q4) ? 1 : 0);
+      const int kind1 = (2 * half + 1 == q4) ? 2 : ((rrev ? 2 * half + 1 > q4 : 2 * half + 1 < q4) ? 1 : 0);
       int mask_h = -1;
       for (int j = 0; j <= T; ++j) {
         if (j < T) {
@@ -523,22 +571,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mask_h = rc.h;
             const float l2 = rc.l2;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) G[jj] = REV ? lam_pow(l2, jj) : lam_pow(l2, 15 - jj);
+            for (int jj = 0; jj < 16; ++jj) G[jj] = rrev ? lam_pow(l2, jj) : lam_pow(l2, 15 - jj);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int ch = 4 * half + c;
-              if (!REV) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
+              if (!rrev) F[c] = (ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f;
               else F[c] = (ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f;
             }
             if (hm == 0 || hm == 1) {
 #pragma unroll
               for (int cc = 0; cc < 2; ++cc) {
                 const int ch = 4 * half + 2 * hm + cc;
-                const float fv = !REV ? ((ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f)
+                const float fv = !rrev ? ((ch < dch) ? lam_pow(l2, row - 16 * ch - 15) : 0.f)
                                       : ((ch > dch) ? lam_pow(l2, 16 * ch - row) : 0.f);
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
-                  const float dg = !REV ? ((jj <= tt) ? lam_pow(l2, tt - jj) : 0.f)
+                  const float dg = !rrev ? ((jj <= tt) ? lam_pow(l2, tt - jj) : 0.f)
                                         : ((jj >= tt) ? lam_pow(l2, jj - tt) : 0.f);
                   MX[cc][jj] = (ch == dch) ? dg : fv * G[jj];
                 }
@@ -608,7 +656,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int bh = rb.bh, slice = rb.slice, blk = rb.blk;
           const float out_l2 = rb.l2;
           const int r = min(BT, N - blk * BT);
-          const float a = REV ? (row < r ? lam_pow(out_l2, r - 1 - row) : 0.f) : lam_pow(out_l2, row + 1);
+          const float a = rrev ? (row < r ? lam_pow(out_l2, r - 1 - row) : 0.f) : lam_pow(out_l2, row + 1);
           uint8_t* sO = smem + L::OFF_O + (i % OS) * L::O_BYTES;
           const bool storer = (half == 0 && lane == 0);
           if (warp == LA2_TRW) TR(2, i, 3);
@@ -671,7 +719,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (half == 0 && lane == 0) tma_store_wait_all0();
     }
-  } else if (warp < WY) {
+  } else if (warp < WY && !dqr) {
     // ------------------------------------------------------------- state warps
     const int q4 = warp & 3;  // warps 10-13 -> quarters 2,3,0,1
     const int row = q4 * 32 + lane;  // token row for K~
@@ -748,6 +796,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const BlkRec rc = recs[0];
       load_state(rc.bh, rc.slice, rc.pos);
     }
+    // Forward with stored states (p.store_states, d = 64 F passes): the bf16 operand copy
+    // of KV_{blk-1} that Oe_blk reads is also written to kv_blocks[bh][blk] by TMA (the
+    // backward triple's dQ CTA reads it back instead of replaying the recurrence).
+    const bool st_states = !SO && !REV && DK == 64 && p.store_states;
+    auto store_block_state = [&](int j) {
+      named_bar_sync(5, 128);  // all four warps' rows of the operand are written
+      if (warp == W0 && lane == 0) {
+        const BlkRec rn = recs[j & 7];
+        tma_store_3d(&tm_v1, sKVb, 0, rn.blk * DK, rn.bh);
+        tma_store_commit();
+      }
+    };
     if (!SO) {
       if (has_kv) {
 #pragma unroll
@@ -756,6 +816,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
+      if (st_states && T > 0) store_block_state(0);
     }
     for (int j = 0; j <= T; ++j) {
       if (j < T) {
@@ -822,6 +883,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
           if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (GW) named_bar_sync(5, 128);
+          if (st_states) {  // the previous block's state store has read the operand buffer
+            if (warp == W0 && lane == 0) tma_store_wait_read<0>();
+            named_bar_sync(5, 128);
+          }
           if (warp == W0) TR(3, i, 7);
           if (has_kv) {
 #pragma unroll
@@ -830,10 +895,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
+          if (st_states && j < T) store_block_state(j);
         }
         if (warp == W0) TR(3, i, 5);
       }
     }
+    if (st_states && warp == W0 && lane == 0) tma_store_wait_all0();
   } else if (warp == WC && L::CW) {
     // ------------------------------------------------------------- V~ copy warp
     // V~_j = c . V_j (c_t = lam^(r-1-t), rev: lam^(t+1)), the fold operand of dKV_j. Off
@@ -969,8 +1036,9 @@ int set_tuning(int key, int value) {
 }
 
 template <int DK, bool REV, bool SO, int CM>
-static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullptr) {
-  using L = TcLayout<DK, SO>;
+static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullptr,
+                       const FArgs* a2 = nullptr) {
+  using L = TcLayout<DK, SO, CM == 4>;
   auto kern = la2_tc_kernel<DK, REV, SO, CM>;
   cudaError_t e = cudaSuccess;
   static int attr_dev = -1;  // attributes are per device; set once (they cost a driver call)
@@ -1004,6 +1072,16 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   }
   if (SO) { mq = mk; mo = mv; mq1 = mk; mo1 = mv; }
   if (CM != 3) { mk1 = mk; mv1 = mv; }
+  // per-block states (forward store / triple load): tm_v1; the triple's dQ output: tm_k1
+  const void* kvb = (CM == 4) ? (a2 ? a2->kv_blocks : nullptr) : a.kv_blocks;
+  const bool store_states = (CM == 0 && !REV && !SO && DK == 64 && kvb != nullptr);
+  if (CM == 4 || store_states) {
+    if (kvb == nullptr) return set_error(LA2_ERR_VALUE, "per-block state buffer is null");
+    const int nblk = (a.N + BT - 1) / BT;
+    int rc = make_tmap(&mv1, kvb, DK, nblk * DK, BH, DK);
+    if (rc == 0 && CM == 4) rc = make_tmap(&mk1, a2->o, DK, a.N, BH, 32);
+    if (rc != 0) return set_error(LA2_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state blocks / dQ");
+  }
   FParams p;
   p.N = a.N;
   p.H = a.H;
@@ -1017,12 +1095,13 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : static_cast<long long>(DK) * a.dv;
   p.kv_out_rs = a.kv_out_rs ? a.kv_out_rs : a.dv;
   p.accum = a.accum_o;
+  p.store_states = store_states ? 1 : 0;
   p.pf = prefetch_blocks();
   p.hint = l2_hints();
   // persistent schedule: units = independent recurrences (a cluster's pair counts once)
-  constexpr int CS = (CM == 3) ? 4 : (CM ? 2 : 1);
+  constexpr int CS = (CM == 3) ? 4 : ((CM == 4) ? 3 : (CM ? 2 : 1));
   p.nsl = a.dv / DVS;
-  p.units = (CM == 2) ? BH : ((CM == 1 || CM == 3) ? BH * p.nsl / 2 : BH * p.nsl);
+  p.units = (CM == 2 || CM == 4) ? BH : ((CM == 1 || CM == 3) ? BH * p.nsl / 2 : BH * p.nsl);
   p.P = p.units;
   p.ws = nullptr;
   p.flags = nullptr;
@@ -1132,6 +1211,13 @@ int launch_tc_pair(const FArgs& adv, const FArgs& adk, cudaStream_t st) {
     return launch_tc_t<64, true, false, 0>(adv, st);
   }
   return launch_tc_t<64, true, false, 2>(adv, st, &adk);
+}
+
+// d = dv = 64 with the forward's per-block states: dV, dK and dQ as one 3-CTA cluster per
+// head walking the blocks in reverse (ranks 0-1 the dV / dK scans, rank 2 the stateless dQ).
+int launch_tc_triple(const FArgs& adv, const FArgs& adk, const FArgs& adq, cudaStream_t st) {
+  if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
+  return launch_tc_t<64, true, false, 4>(adv, st, &adk, &adq);
 }
 
 // d = dv = 128: the dV and dK reverse scans as one 4-CTA cluster per unit -- each pass

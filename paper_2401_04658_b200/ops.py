@@ -280,6 +280,56 @@ def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
     return o, kv_out
 
 
+def states_eligible(q: torch.Tensor, v: torch.Tensor) -> bool:
+    """Shapes whose backward can use stored per-block states (la2_forward_states /
+    la2_backward_states, include/la2.h): bf16, d = dv = 64."""
+    return q.dtype == torch.bfloat16 and q.shape[3] == 64 and v.shape[3] == 64
+
+
+def la2_forward_states(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
+                       output_final_state: bool = False):
+    """Forward that also returns the per-block bf16 states ``[B, H, ceil(N/128), d, dv]``
+    (entry i = the state block i read: KV_{i-1}) for :func:`la2_backward_states`.
+    Returns ``(o, kv_out, kv_blocks)``."""
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    if not states_eligible(q, v):
+        raise ValueError("stored per-block states need bf16 with d = dv = 64")
+    dec = _decay(decay, H, q.device)
+    kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
+    kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(v)
+    blocks = torch.empty(B, H, (N + 127) // 128, d, dv, device=q.device, dtype=torch.bfloat16)
+    _lib.call("la2_forward_states", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in),
+              _ptr(kv_out), _ptr(blocks), B, H, N, d, dv, _code(q), _stream(q.device))
+    return o, kv_out, blocks
+
+
+def la2_backward_states(q, k, v, d_out, decay: DecayLike, kv_blocks: torch.Tensor, dkv_in=None,
+                        output_dkv: bool = False):
+    """Backward from the forward's stored per-block states (dQ without replaying the
+    recurrence, in one 3-CTA cluster with the dK / dV reverse scans). Same results as
+    :func:`la2_backward` up to rounding. Returns ``(dq, dk, dv, dkv_out)``."""
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    if not states_eligible(q, v):
+        raise ValueError("stored per-block states need bf16 with d = dv = 64")
+    if d_out.shape != v.shape or d_out.dtype != v.dtype:
+        raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
+    nblk = (N + 127) // 128
+    if (tuple(kv_blocks.shape) != (B, H, nblk, d, dv) or kv_blocks.dtype != torch.bfloat16
+            or not kv_blocks.is_contiguous()):
+        raise ValueError(f"kv_blocks must be a contiguous bf16 tensor of shape {(B, H, nblk, d, dv)}")
+    dec = _decay(decay, H, q.device)
+    dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
+    dkv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_dkv else None
+    q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
+    dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    _lib.call("la2_backward_states", _ptr(q), _ptr(k), _ptr(v), _ptr(d_out), _ptr(dec), _ptr(kv_blocks),
+              _ptr(dq), _ptr(dk), _ptr(dvv), _ptr(dkv_in), _ptr(dkv_out), B, H, N, d, dv, _code(q),
+              _stream(q.device))
+    return dq, dk, dvv, dkv_out
+
+
 def _head_stride(t: torch.Tensor) -> Optional[int]:
     """Element stride between consecutive (b, h) rows of a [B,H,N,c] view whose rows are
     contiguous and evenly spaced (la2_forward_strided), else None."""
@@ -433,6 +483,15 @@ def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.T
 
 
 # ------------------------------------------------------------------- autograd
+# d = dv = 64 bf16 training: the forward stores its per-block states and the backward runs
+# dQ / dK / dV as one 3-CTA cluster (la2_forward_states / la2_backward_states); False: the
+# backward replays the recurrence for dQ (la2_backward)
+STORED_STATES = True
+# ... for sequences of at least this many tokens. Measured (B=8 H=16 d=64, one B200,
+# profiles/r2b_bench_c2.json vs r2a): the triple is 1-4 % faster from N = 16K up and equal at
+# 8K, but slower below, where the replay path overlaps its dQ scan with the dK/dV pair on
+# partitioned SMs and the 3-CTA clusters (45 of them: 135 of 148 SMs) quantise badly.
+STORED_STATES_MIN_N = 16384
 class LightningAttn2Fn(torch.autograd.Function):
     """Autograd wrapper: saves q, k, v, decay (and the initial state) and
     recomputes the KV state in backward -- no per-block checkpoints, matching
@@ -442,9 +501,17 @@ class LightningAttn2Fn(torch.autograd.Function):
     def forward(ctx, q, k, v, decay, initial_state, output_final_state, seq_split):
         B, H, N, d = q.shape
         g = split_factor(B, H, N, d, v.shape[3], q.dtype) if seq_split == "auto" else int(seq_split)
+        ctx.stored = False
         if g > 1:
             o, kv_out, prefix = split_forward(q, k, v, decay, g, kv_in=initial_state,
                                               output_final_state=output_final_state)
+        elif (STORED_STATES and N >= STORED_STATES_MIN_N and states_eligible(q, v)
+              and any(ctx.needs_input_grad[:3])):
+            # d = 64: keep the per-block states (half a tensor of HBM) so the backward's dQ
+            # needs no replay scan and shares the dK / dV passes' reads
+            o, kv_out, prefix = la2_forward_states(q, k, v, decay, kv_in=initial_state,
+                                                   output_final_state=output_final_state)
+            ctx.stored = True
         else:
             o, kv_out = la2_forward(q, k, v, decay, kv_in=initial_state,
                                     output_final_state=output_final_state)
@@ -466,6 +533,9 @@ class LightningAttn2Fn(torch.autograd.Function):
         if ctx.g > 1:
             dq, dk, dv, dkv = split_backward(q, k, v, d_o.to(q.dtype).contiguous(), decay, ctx.g, prefix,
                                              dkv_in=d_final, output_dkv=ctx.want_state_grad)
+        elif ctx.stored:
+            dq, dk, dv, dkv = la2_backward_states(q, k, v, d_o.to(q.dtype), decay, prefix,
+                                                  dkv_in=d_final, output_dkv=ctx.want_state_grad)
         else:
             dq, dk, dv, dkv = la2_backward(q, k, v, d_o.to(q.dtype), decay, kv_in=initial_state,
                                            dkv_in=d_final, output_dkv=ctx.want_state_grad)

@@ -924,3 +924,74 @@ def test_launch_log_records_each_kernel():
     # off: nothing is logged
     ops.la2_forward(q, k, v, 0.9)
     assert ops.read_launch_log() == []
+
+
+# ------------------------------------------------ stored per-block states (d = 64)
+@pytest.mark.parametrize("B,H,N", [(1, 3, 700), (2, 40, 1000), (4, 40, 2048), (1, 2, 128), (1, 1, 1)])
+def test_backward_from_stored_states(B, H, N):
+    """la2_forward_states stores KV_{i-1} per 128-token block (bf16) and computes the same
+    o as la2_forward (bitwise); la2_backward_states (dV, dK and a stateless dQ in one 3-CTA
+    cluster) matches the oracle, with kv_in in the forward and dkv_in / dkv_out in the
+    backward. B*H = 80/160 > 49 co-resident triples exercises the persistent hand-off."""
+    from paper_2401_04658_b200 import ops
+    q, k, v, do = inputs(B, H, N, 64, 64, torch.bfloat16, seed=N + H)
+    decay = [[0.5, 0.9, 0.99, 0.999, 0.9999, 1.0][h % 6] for h in range(H)]
+    g = torch.Generator().manual_seed(11)
+    kv0 = (torch.rand(B, H, 64, 64, generator=g, dtype=torch.float64) - 0.5).float()
+    dkv0 = (torch.rand(B, H, 64, 64, generator=g, dtype=torch.float64) - 0.5).float()
+    qd, kd, vd, dod = gpu(q, k, v, do)
+    o_ref, kv_ref = ops.la2_forward(qd, kd, vd, decay, kv_in=kv0.to(DEV), output_final_state=True)
+    o, kv, blocks = ops.la2_forward_states(qd, kd, vd, decay, kv_in=kv0.to(DEV), output_final_state=True)
+    assert torch.equal(o, o_ref) and torch.equal(kv, kv_ref)
+    nblk = (N + 127) // 128
+    assert blocks.shape == (B, H, nblk, 64, 64)
+    # stored state i = the state entering block i
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    S0, T0 = kv0.double().numpy(), dkv0.double().numpy()
+    for b, h in ((0, 0), (B - 1, H - 1)):
+        for i in sorted({0, nblk // 2, nblk - 1}):
+            _, st = port.bhnd_forward(Q[b:b + 1, h:h + 1, :128 * i], K[b:b + 1, h:h + 1, :128 * i],
+                                      V[b:b + 1, h:h + 1, :128 * i], [decay[h]],
+                                      kv_in=S0[b:b + 1, h:h + 1]) if i else (None, S0[b:b + 1, h:h + 1])
+            assert rel(blocks[b, h, i], st[0, 0]) <= BF16_TOL, (b, h, i)
+    dq, dk, dv_, dkv = ops.la2_backward_states(qd, kd, vd, dod, decay, blocks, dkv_in=dkv0.to(DEV),
+                                               output_dkv=True)
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay)
+    rdkv = np.empty_like(S0)
+    for b in range(B):
+        for h in range(H):
+            lam = decay[h]
+            a = lam ** (np.arange(N) + 1.0)
+            c = lam ** (N - 1.0 - np.arange(N))
+            rq[b, h] += (DO[b, h] * a[:, None]) @ S0[b, h].T
+            rk[b, h] += (V[b, h] * c[:, None]) @ T0[b, h].T
+            rv[b, h] += (K[b, h] * c[:, None]) @ T0[b, h]
+            rdkv[b, h] = lam ** N * T0[b, h] + (Q[b, h] * a[:, None]).T @ DO[b, h]
+    errs = {"dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv), "dkv": rel(dkv, rdkv)}
+    print((B, H, N), errs)
+    assert max(errs.values()) <= BF16_TOL, errs
+    # the pair and the replay path agree with the triple up to rounding
+    dq2, dk2, dv2, _ = ops.la2_backward(qd, kd, vd, dod, decay, kv_in=kv0.to(DEV), dkv_in=dkv0.to(DEV))
+    assert torch.equal(dk, dk2) and torch.equal(dv_, dv2)
+    assert rel(dq, to64(dq2)) <= 1e-2
+
+
+def test_autograd_uses_stored_states():
+    """lightning_attn2 training at d = 64 runs the forward with stored states and the
+    backward triple (launch log), and matches the oracle."""
+    from paper_2401_04658_b200 import ops
+    q, k, v, do = inputs(1, 4, ops.STORED_STATES_MIN_N, 64, 64, torch.bfloat16, seed=3)
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    ops.launch_log(16)
+    try:
+        o = la2.lightning_attn2(qg, kg, vg, 0.999)
+        o.backward(do.to(DEV))
+        names = [r["kernel"] for r in ops.read_launch_log()]
+    finally:
+        ops.launch_log(0)
+    assert names == ["la2_tc_kernel<64,0,0,0>", "la2_tc_kernel<64,1,0,4>"], names
+    Q, K, V, DO = map(to64, (q, k, v, do))
+    ro, _ = port.bhnd_forward(Q, K, V, [0.999] * 4)
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, [0.999] * 4)
+    errs = {"o": rel(o, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
+    assert max(errs.values()) <= BF16_TOL, errs
