@@ -122,6 +122,59 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// ------------------------------------------------ distributed shared memory (cluster)
+// Address of the same-offset shared location in cluster CTA `rank`.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// Arrive on an mbarrier of another CTA of the cluster (address from mapa_shared); release
+// at cluster scope orders this thread's preceding shared::cluster stores before it.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// Make this thread's generic-proxy shared::cluster stores visible to the async proxy
+// (the tensor core of the CTA that owns the memory).
+#ifndef LA2_FENCE_CLUSTER
+#define LA2_FENCE_CLUSTER 1
+#endif
+__device__ __forceinline__ void fence_proxy_async_cluster() {
+#if LA2_FENCE_CLUSTER
+  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+#endif
+}
+// Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory to a cluster peer's
+// (dst and bar are peer addresses from mapa_shared); completes `bytes` of transaction
+// count on the peer's mbarrier -- asynchronous, like a TMA load into the peer.
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                                  uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+// mbarrier wait with cluster-scope acquire (the phase may be completed by remote arrivals
+// whose writes this thread then reads / hands to the tensor core).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@p bra.uni DONEC;\n\t"
+      "bra.uni LAB_WAITC;\n\t"
+      "DONEC:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(LA2_MBAR_HINT)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -314,6 +367,16 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1u) << 46;  // descriptor version (sm_100)
   d |= static_cast<uint64_t>(2u) << 61;  // SWIZZLE_128B
+  return d;
+}
+// SW64 variant (64-byte swizzle atom: 8 rows x 64 bytes, chunk' = chunk ^ ((row >> 1) & 3)).
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;  // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(4u) << 61;  // SWIZZLE_64B
   return d;
 }
 // Instruction descriptor: bf16 x bf16 -> fp32, dense.

@@ -54,6 +54,13 @@ constexpr int WC = WY + 1;      // V~ copy warp
 // Group waits: one warp of a group polls an mbarrier, its partners sleep in a named
 // barrier (fewer spinning warps: less issue pressure and power, one more bar.sync).
 constexpr bool GW = (LA2_GROUP_WAIT != 0);
+// Backward pair / triple (d = dv = 64): the dV pass's state dKV and the dK pass's state
+// dKV^T are the same matrix, so ranks 0 and 1 share ONE recurrence -- each computes the
+// fold and the fp32 update for 32 of its 64 columns and writes its half of the bf16
+// operand into both CTAs' shared memory (the dK pass reads it K-major, i.e. transposed).
+#ifndef LA2_SPLIT_STATE
+#define LA2_SPLIT_STATE 1
+#endif
 
 #ifndef LA2_SO_NS
 #define LA2_SO_NS 4
@@ -78,9 +85,13 @@ struct TcLayout {
   static constexpr int OFF_S = OFF_V + NS * V_BYTES;
   static constexpr int OFF_KT = OFF_S + NS * S_BYTES;
   static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
-  static constexpr int OFF_O = OFF_KV + KV_BYTES;
+  // second bf16 state-operand buffer of the backward pair / triple's shared recurrence
+  // (LA2_SPLIT_STATE): the triple's ranks 0-1 use their (otherwise idle) state-tile ring
+  static constexpr bool KV2 = (DK == 64) && !SO && !TRI;
+  static constexpr int OFF_O = OFF_KV + (KV2 ? 2 : 1) * KV_BYTES;
+  static constexpr int OFF_KV2 = TRI ? OFF_S : OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
   static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
@@ -104,7 +115,7 @@ struct TcLayout {
                        B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEFULL = B_OFULL + 2,
                        B_OEMPTY = B_OEFULL + 2, B_KTREADY = B_OEMPTY + 2, B_KTFREE = B_KTREADY + KTS,
                        B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 2,
-                       B_KVREADY = B_DKVEMPTY + 2, B_COUNT = B_KVREADY + 1;
+                       B_KVREADY = B_DKVEMPTY + 2, B_KVFREE = B_KVREADY + 2, B_COUNT = B_KVFREE + 2;
   static_assert(B_COUNT * 8 + 16 <= BAR_BYTES, "barrier area");
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
@@ -157,6 +168,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const bool dqr = (CM == 4) && (crank == 2);  // the triple's stateless dQ CTA
   const bool rrev = REV && !dqr;               // scan direction of this CTA's masks / factors
   const bool sib = ((CM == 2 || CM == 4) && (crank == 1)) || ((CM == 3) && pair == 1);  // sibling pass
+  // shared recurrence of the backward pair / triple (LA2_SPLIT_STATE): ranks 0-1 fold
+  // Q^T (c . dO) (Q at OFF_K, dO at OFF_V in both), columns [32 crank, 32 crank + 32)
+  constexpr bool SPLIT = (CM == 2 || CM == 4) && (LA2_SPLIT_STATE != 0);
+  constexpr int KVC = SPLIT ? 32 : DVS;               // state columns held by this CTA
+  const int kc0 = SPLIT ? 32 * static_cast<int>(crank) : 0;
   const CUtensorMap* mq = (sib || dqr) ? &tm_q1 : &tm_q;  // dqr: its own copy of V (tm_q1)
   const CUtensorMap* mo = dqr ? &tm_k1 : (sib ? &tm_o1 : &tm_o);  // dqr: dQ through tm_k1
   const CUtensorMap* mk = (CM == 3 && sib) ? &tm_k1 : &tm_k;
@@ -167,8 +183,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int offq = dqr ? L::OFF_V : L::OFF_Q;
   const int offk = dqr ? L::OFF_K : (((CM == 2 || CM == 4) && sib) ? L::OFF_V : L::OFF_K);
   const int offv = dqr ? L::OFF_Q : (((CM == 2 || CM == 4) && sib) ? L::OFF_K : L::OFF_V);
-  const int kv_in_T = sib ? 1 : p.kv_in_T;          // the dK pass carries dKV^T
-  float* const kv_out = (sib || dqr) ? nullptr : p.kv_out;
+  const int kv_in_T = SPLIT ? 0 : (sib ? 1 : p.kv_in_T);  // the dK pass carries dKV^T
+  float* const kv_out = (SPLIT ? dqr : (sib || dqr)) ? nullptr : p.kv_out;
+  const int offsk = SPLIT ? L::OFF_K : offk;  // the state chain's k / v tiles
+  const int offsv = SPLIT ? L::OFF_V : offv;
   const int N = p.N;
   const int nblk = (N + BT - 1) / BT;
   const int cid = blockIdx.x / CS;                  // this CTA's (cluster's) work range
@@ -206,7 +224,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&bars[L::B_DKVFULL + b], 1);
       mbar_init(&bars[L::B_DKVEMPTY + b], 4);
     }
-    mbar_init(&bars[L::B_KVREADY], 4);
+    // SPLIT: per operand buffer, both CTAs' state warps / both CTAs' Oe commits
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[L::B_KVREADY + b], 4);  // SPLIT: + the peer's half by bulk copy (tx bytes)
+      mbar_init(&bars[L::B_KVFREE + b], 2);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -503,7 +525,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (leader) {
           // dKV = K^T (c . V): A = K^T (MN-major view of the K stage), B = V~ (MN-major)
           const uint64_t vt_d = adv(dKT0, kt * L::V_BYTES);
-          const uint64_t kA = sdesc_sw128(smem_u32(smem + offk + s * L::K_BYTES), REGION, 1024);
+          const uint64_t kA = sdesc_sw128(smem_u32(smem + offsk + s * L::K_BYTES), REGION, 1024);
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
             umma_bf16_ss(tKV + db * 64, adv(kA, kk * 2048), adv(vt_d, kk * 2048), ID_KV, kk > 0);
@@ -513,24 +535,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         __syncwarp();
         if (!SO) {
-          mbar_wait(&bars[L::B_KVREADY], i & 1);
+          // SPLIT: KV_{i-1} sits in operand buffer i & 1, half of it written by the peer
+          if (SPLIT) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
+          else mbar_wait(&bars[L::B_KVREADY], i & 1);
           if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
           if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           TR(1, i, 4);
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES);
+            if (SPLIT) {
+              // the shared operand: two [64 d rows][32 dv cols] SW64 halves (one per CTA,
+              // 4 KB apart). dV pass (rank 0): Oe = K dKV, B MN-major (K = d rows, 16 per
+              // step = 1024 B; the halves are the two N atoms, LBO 4096). dK pass (rank 1):
+              // Oe = V dKV^T, the same bytes K-major (N = d rows; K = dv: 32 B steps inside
+              // a half, then the other half).
+              const uint32_t kvb = smem_u32(smem + ((i & 1) ? L::OFF_KV2 : L::OFF_KV));
+              if (crank == 0) {
+                const uint64_t dm = sdesc_sw64(kvb, 4096, 512);
 #pragma unroll
-            for (int kk = 0; kk < DK / 16; ++kk)
-              umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
-                           adv(dKV0, kk * 2048), ID_O, kk > 0);
+                for (int kk = 0; kk < DK / 16; ++kk)
+                  umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dm, kk * 1024), ID_O,
+                               kk > 0);
+              } else {
+                const uint64_t dk = sdesc_sw64(kvb, 16, 512);
+#pragma unroll
+                for (int kk = 0; kk < DK / 16; ++kk)
+                  umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
+                               adv(dk, (kk >> 1) * 4096 + (kk & 1) * 32), ID_OS, kk > 0);
+              }
+            } else {
+              const uint64_t kvd = dKV0;
+#pragma unroll
+              for (int kk = 0; kk < DK / 16; ++kk)
+                umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
+                             adv(kvd, kk * 2048), ID_O, kk > 0);
+            }
             umma_commit(&bars[L::B_OEFULL + db]);
+            if (SPLIT) umma_commit_mc(&bars[L::B_KVFREE + (i & 1)], 0x3);  // both CTAs' copies read
             commit_empty(s);
           }
           __syncwarp();
         }
         TR(1, i, 6);
       }
+      // SPLIT: the last Oe's commits (ours and the peer's) have landed in this CTA's
+      // KVFREE barrier before teardown (no tcgen05 arrive may target an exited CTA)
+      if (SPLIT && !dqr && T > 0) mbar_wait(&bars[L::B_KVFREE + ((T - 1) & 1)], ((T - 1) >> 1) & 1);
     }
   } else if (warp < W0) {
     // --------------------------------------------------------------- row warps
@@ -728,27 +779,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool has_kv = (DK == 128) || (lane < 16);
     const int kvrow = (DK == 128) ? row : (q4 * 16 + lane);
     const int dvt = p.dv_total;
-    float kv[DVS];
+    float kv[KVC];
+    // SPLIT: the peer's operand buffer and KVREADY barrier (this CTA writes half of both)
+    const uint32_t peer = static_cast<uint32_t>(crank) ^ 1u;
+    // (operand buffer b at OFF_KV / OFF_KV2 with its KVREADY barrier; KV_m goes to (m + 1) & 1)
+    const uint32_t r_base = SPLIT ? mapa_shared(smem_u32(smem), peer) : 0u;
+    const uint32_t r_kvready0 = SPLIT ? mapa_shared(smem_u32(&bars[L::B_KVREADY]), peer) : 0u;
     // Segment start: the caller's initial state (or zero) at scan position 0, else the
     // state the previous work range published for this unit.
     auto load_state = [&](int bh, int slice, int pos) {
 #pragma unroll
-      for (int j = 0; j < DVS; ++j) kv[j] = 0.f;
+      for (int j = 0; j < KVC; ++j) kv[j] = 0.f;
       if (pos == 0) {
         if (p.kv_in != nullptr && has_kv) {
           const size_t sbase = static_cast<size_t>(bh) * p.kv_in_bhs;
-          const int c0 = slice * DVS;
+          const int c0 = slice * DVS + kc0;
           if (!kv_in_T) {
             const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * p.kv_in_rs + c0;
 #pragma unroll
-            for (int j = 0; j < DVS; j += 4) {
+            for (int j = 0; j < KVC; j += 4) {
               float4 w = *reinterpret_cast<const float4*>(src + j);
               kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
             }
           } else {
             // state stored transposed: element (r, c) at c * rs + r
 #pragma unroll
-            for (int j = 0; j < DVS; ++j)
+            for (int j = 0; j < KVC; ++j)
               kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * p.kv_in_rs + kvrow];
           }
         }
@@ -760,7 +816,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const float4* src = reinterpret_cast<const float4*>(
               p.ws + (static_cast<size_t>(slot) * DK + kvrow) * DVS);
 #pragma unroll
-          for (int j = 0; j < DVS; j += 4) {
+          for (int j = 0; j < KVC; j += 4) {
             float4 w = __ldcg(src + j / 4);
             kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
           }
@@ -773,9 +829,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (pos == nblk - 1) {
         if (kv_out != nullptr && has_kv) {
           float* dst = kv_out + static_cast<size_t>(bh) * p.kv_out_bhs +
-                       static_cast<size_t>(kvrow) * p.kv_out_rs + slice * DVS;
+                       static_cast<size_t>(kvrow) * p.kv_out_rs + slice * DVS + kc0;
 #pragma unroll
-          for (int j = 0; j < DVS; j += 4)
+          for (int j = 0; j < KVC; j += 4)
             *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
         }
       } else {
@@ -783,7 +839,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (has_kv) {
           float4* dst = reinterpret_cast<float4*>(p.ws + (static_cast<size_t>(slot) * DK + kvrow) * DVS);
 #pragma unroll
-          for (int j = 0; j < DVS; j += 4) __stcg(dst + j / 4, make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]));
+          for (int j = 0; j < KVC; j += 4) __stcg(dst + j / 4, make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]));
         }
         __threadfence();
         named_bar_sync(5, 128);
@@ -808,14 +864,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tma_store_commit();
       }
     };
-    if (!SO) {
-      if (has_kv) {
+    // the bf16 operand copy of the state (SPLIT: this CTA's half, into both CTAs)
+    auto write_operand = [&](int b) {
+      if constexpr (SPLIT) {
+        // this CTA's 32 columns of row kvrow are one contiguous 64-byte half of the
+        // swizzled 128-byte row; written here, then bulk-copied into the peer's buffer
+        // (completing 64 tx bytes of the peer's KVREADY; its W0 expects all 64 rows)
+        // this CTA's half: [64 d rows][32 cols] SW64 at +4096 * crank; a warp's 16 rows
+        // are one contiguous KB, bulk-copied into the peer's buffer (completing tx bytes
+        // of the peer's KVREADY, whose W0 expects all 4 KB)
+        uint8_t* hb = smem + (b ? L::OFF_KV2 : L::OFF_KV) + 4096 * static_cast<int>(crank);
+        if (has_kv) {
+          uint8_t* rp = hb + kvrow * 64;
 #pragma unroll
-        for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
+          for (int c = 0; c < 4; ++c) {
+            uint4 w;
+            w.x = pack_bf16x2(kv[8 * c + 0], kv[8 * c + 1]);
+            w.y = pack_bf16x2(kv[8 * c + 2], kv[8 * c + 3]);
+            w.z = pack_bf16x2(kv[8 * c + 4], kv[8 * c + 5]);
+            w.w = pack_bf16x2(kv[8 * c + 6], kv[8 * c + 7]);
+            *reinterpret_cast<uint4*>(rp + ((c ^ ((kvrow >> 1) & 3)) * 16)) = w;
+          }
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t off = static_cast<uint32_t>(hb - smem) + q4 * 16 * 64;
+          bulk_copy_to_peer(r_base + off, smem + off, 16 * 64, r_kvready0 + 8u * b);
+          if (warp == W0) mbar_arrive_expect_tx(&bars[L::B_KVREADY + b], DK * 64);
+          else mbar_arrive(&bars[L::B_KVREADY + b]);
+        }
+      } else {
+        if (has_kv) {
+#pragma unroll
+          for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
+    };
+    if (!SO) {
+      write_operand(0);
       if (st_states && T > 0) store_block_state(0);
     }
     for (int j = 0; j <= T; ++j) {
@@ -832,8 +922,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const float c = REV ? lam_pow(rc.l2, row + 1) : (row < r ? lam_pow(rc.l2, r - 1 - row) : 0.f);
           if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
           if (warp == W0) TR(3, j, 1);
-          scale_row_copy<64>(smem + offv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
-                             row, c);
+          if (SPLIT)
+            scale_row_copy_half(smem + offsv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES, row,
+                                static_cast<int>(crank), c);
+          else
+            scale_row_copy<64>(smem + offsv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
+                               row, c);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[L::B_KTREADY + kt]);
@@ -856,9 +950,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (warp == W0) TR(3, i, 4);
         tc_fence_after();
 #pragma unroll
-        for (int q = 0; q < DVS / 32; ++q) {  // two 32-column loads: half the round trips
+        for (int q = 0; q < KVC / 32; ++q) {  // 32-column loads: half the round trips
           uint32_t d32[32];
-          tmem_ld32_raw(tbase + L::T_KV + db * 64 + lane_off + q * 32, d32);
+          tmem_ld32_raw(tbase + L::T_KV + db * 64 + lane_off + kc0 + q * 32, d32);
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll
@@ -881,20 +975,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (!SO) {
           // the bf16 copy of KV_{i-1} is the B operand of Oe_i: wait until it is consumed
-          if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
+          // (SPLIT: by both CTAs, whose copies this CTA writes)
+          // (SPLIT: KV_i goes to buffer (i + 1) & 1, last read by Oe_{i-1} in both CTAs)
+          if (SPLIT) {
+            if (i >= 1) mbar_wait(&bars[L::B_KVFREE + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          }
+          else if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (GW) named_bar_sync(5, 128);
           if (st_states) {  // the previous block's state store has read the operand buffer
             if (warp == W0 && lane == 0) tma_store_wait_read<0>();
             named_bar_sync(5, 128);
           }
           if (warp == W0) TR(3, i, 7);
-          if (has_kv) {
-#pragma unroll
-            for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
+          // (SPLIT: no copy after the last block -- nothing reads it, and a bulk copy must
+          // not land in a peer that has already exited)
+          if (!SPLIT || j < T) write_operand((i + 1) & 1);
           if (st_states && j < T) store_block_state(j);
         }
         if (warp == W0) TR(3, i, 5);
@@ -1167,11 +1262,10 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
 }
 
 #ifdef LA2_TRACE
-int set_trace_bwd(long long* buf);
 extern "C" LA2_API int la2_set_trace(long long* buf) {
   cudaError_t e = cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
   if (e != cudaSuccess) return set_cuda_error("la2_set_trace", e);
-  return set_trace_bwd(buf);
+  return 0;
 }
 #endif
 

@@ -16,9 +16,12 @@ static __device__ long long* g_trace = nullptr;  // per translation unit
 constexpr int TR_MAXB = 64, TR_EV = 8;  // roles 0..4
 // TR_INIT caches the buffer pointer (and the "is CTA 0" test) in registers at kernel
 // start: re-reading the __device__ pointer per event put an L2 round trip on every stamp.
+#ifndef LA2_TRB
+#define LA2_TRB 0  // the CTA whose phases are traced
+#endif
 #define TR_INIT                                                                                  \
   long long* const tr_buf =                                                                      \
-      (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_trace : nullptr
+      (blockIdx.x == LA2_TRB && blockIdx.y == 0 && blockIdx.z == 0) ? g_trace : nullptr
 #define TR(role, blk, ev)                                                                        \
   do {                                                                                           \
     if (tr_buf && (blk) < TR_MAXB && (threadIdx.x & 31) == 0)                                    \
@@ -61,6 +64,44 @@ __device__ __forceinline__ void scale_row_copy(const uint8_t* src, uint8_t* dst,
   }
 }
 
+// Half of scale_row_copy<64>: logical 16-byte chunks [4h, 4h+4) of one row (columns
+// 32h..32h+31), scaled by f, into the same chunks of dst.
+__device__ __forceinline__ void scale_row_copy_half(const uint8_t* src, uint8_t* dst, int row, int h,
+                                                    float f) {
+  const uint8_t* sp = src + row * 128;
+  uint8_t* dp = dst + row * 128;
+  uint4 w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = *reinterpret_cast<const uint4*>(sp + (((4 * h + k) ^ (row & 7)) * 16));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t* u = reinterpret_cast<uint32_t*>(&w[k]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __fmul2_rn(unpack_bf16x2(u[e]), make_float2(f, f));
+      u[e] = pack_bf16x2(x.x, x.y);
+    }
+    *reinterpret_cast<uint4*>(dp + (((4 * h + k) ^ (row & 7)) * 16)) = w[k];
+  }
+}
+// store_chunk16_bf16 into this CTA's region and the same-offset region of a cluster peer
+// (remote = mapa_shared of the region's base).
+__device__ __forceinline__ void store_chunk16_bf16_dup(uint8_t* region, uint32_t remote, int row, int q,
+                                                       const float* x) {
+  const uint32_t off = row * 128;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = 2 * q + h;
+    uint4 w;
+    w.x = pack_bf16x2(x[8 * h + 0], x[8 * h + 1]);
+    w.y = pack_bf16x2(x[8 * h + 2], x[8 * h + 3]);
+    w.z = pack_bf16x2(x[8 * h + 4], x[8 * h + 5]);
+    w.w = pack_bf16x2(x[8 * h + 6], x[8 * h + 7]);
+    const uint32_t o = off + ((c ^ (row & 7)) * 16);
+    *reinterpret_cast<uint4*>(region + o) = w;
+    st_cluster_v4(remote + o, w);
+  }
+}
 // Write 16 fp32 values as bf16 into logical chunks 2q, 2q+1 of one SW128 row.
 __device__ __forceinline__ void store_chunk16_bf16(uint8_t* region, int row, int q, const float* x) {
   uint8_t* rp = region + row * 128;

@@ -18,9 +18,15 @@ dev = torch.device('cuda', 0)
 q, k, v = ((torch.rand(B, H, N, D, device=dev) * 2 - 1).bfloat16() for _ in range(3))
 dec = la2.decay_tensor(alibi_decay(H), H, dev)
 buf = torch.zeros(4 * 64 * 8, dtype=torch.int64, device=dev)
-la2.la2_backward(q, k, v, q, dec)
+TRIPLE = os.environ.get("TRACE_TRIPLE") == "1"  # the stored-state dQ/dK/dV triple instead
+if TRIPLE:
+    _, _, blocks = la2.ops.la2_forward_states(q, k, v, dec)
+    bwd = lambda: la2.ops.la2_backward_states(q, k, v, q, dec, blocks)  # noqa: E731
+else:
+    bwd = lambda: la2.la2_backward(q, k, v, q, dec)  # noqa: E731
+bwd()
 lib.la2_set_trace(buf.data_ptr())
-la2.la2_backward(q, k, v, q, dec)
+bwd()
 torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(4, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
