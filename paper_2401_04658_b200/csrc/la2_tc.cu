@@ -378,6 +378,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K (K-major)
     constexpr uint32_t ID_O = idesc_bf16(128, DVS, 0, 1);  // P/Q (K-major) x V/KV (MN-major)
     constexpr uint32_t ID_KV = idesc_bf16(DK, DVS, 1, 1);  // K~^T (MN-major) x V (MN-major)
+    // SPLIT: this CTA's 32 state columns; V~ is a compact [128][32] SW64 tile
+    constexpr uint32_t ID_KV32 = idesc_bf16(DK, 32, 1, 1);
     const bool leader = (lane == 0);
     const uint32_t tOE = tbase + L::T_OE, tKV = tbase + L::T_KV;
     // descriptor bases (start address is in 16-byte units in the low bits)
@@ -524,11 +526,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         if (leader) {
           // dKV = K^T (c . V): A = K^T (MN-major view of the K stage), B = V~ (MN-major)
-          const uint64_t vt_d = adv(dKT0, kt * L::V_BYTES);
+          const uint64_t vt_d = SPLIT ? sdesc_sw64(smem_u32(smem + L::OFF_KT + kt * L::V_BYTES), 4096, 512)
+                                      : adv(dKT0, kt * L::V_BYTES);
           const uint64_t kA = sdesc_sw128(smem_u32(smem + offsk + s * L::K_BYTES), REGION, 1024);
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
-            umma_bf16_ss(tKV + db * 64, adv(kA, kk * 2048), adv(vt_d, kk * 2048), ID_KV, kk > 0);
+            umma_bf16_ss(tKV + db * 64, adv(kA, kk * 2048), adv(vt_d, kk * (SPLIT ? 1024 : 2048)),
+                         SPLIT ? ID_KV32 : ID_KV, kk > 0);
           umma_commit(&bars[L::B_DKVFULL + db]);
           umma_commit(&bars[L::B_KTFREE + kt]);
           if (SO) commit_empty(s);
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
           if (warp == W0) TR(3, j, 1);
           if (SPLIT)
-            scale_row_copy_half(smem + offsv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES, row,
+            scale_row_copy_half_sw64(smem + offsv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES, row,
                                 static_cast<int>(crank), c);
           else
             scale_row_copy<64>(smem + offsv + s * L::V_BYTES, smem + L::OFF_KT + kt * L::V_BYTES,
@@ -952,7 +956,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < KVC / 32; ++q) {  // 32-column loads: half the round trips
           uint32_t d32[32];
-          tmem_ld32_raw(tbase + L::T_KV + db * 64 + lane_off + kc0 + q * 32, d32);
+          tmem_ld32_raw(tbase + L::T_KV + db * 64 + lane_off + q * 32, d32);
           tmem_ld_wait();
           if (has_kv) {
 #pragma unroll

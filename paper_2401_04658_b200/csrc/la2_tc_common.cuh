@@ -84,6 +84,26 @@ __device__ __forceinline__ void scale_row_copy_half(const uint8_t* src, uint8_t*
     *reinterpret_cast<uint4*>(dp + (((4 * h + k) ^ (row & 7)) * 16)) = w[k];
   }
 }
+// scale_row_copy_half into a compact [rows][32] SW64 tile (64-byte rows, chunk' = chunk ^
+// ((row >> 1) & 3)): the N = 32 B operand of the shared-recurrence fold.
+__device__ __forceinline__ void scale_row_copy_half_sw64(const uint8_t* src, uint8_t* dst, int row, int h,
+                                                         float f) {
+  const uint8_t* sp = src + row * 128;
+  uint8_t* dp = dst + row * 64;
+  uint4 w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = *reinterpret_cast<const uint4*>(sp + (((4 * h + k) ^ (row & 7)) * 16));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t* u = reinterpret_cast<uint32_t*>(&w[k]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __fmul2_rn(unpack_bf16x2(u[e]), make_float2(f, f));
+      u[e] = pack_bf16x2(x.x, x.y);
+    }
+    *reinterpret_cast<uint4*>(dp + ((k ^ ((row >> 1) & 3)) * 16)) = w[k];
+  }
+}
 // store_chunk16_bf16 into this CTA's region and the same-offset region of a cluster peer
 // (remote = mapa_shared of the region's base).
 __device__ __forceinline__ void store_chunk16_bf16_dup(uint8_t* region, uint32_t remote, int row, int q,
