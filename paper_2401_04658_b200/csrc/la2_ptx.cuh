@@ -161,6 +161,16 @@ __device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, const vo
       "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
       : "memory");
 }
+// Asynchronous 16-byte store into a cluster peer's shared memory that completes 16 bytes of
+// transaction count on the peer's mbarrier (both addresses from mapa_shared): the data is
+// visible to whoever waits on that barrier phase, no fences or release on this side.
+__device__ __forceinline__ void st_async_peer(uint32_t dst_cluster, const uint4& v, uint32_t bar_cluster) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          dst_cluster),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar_cluster)
+      : "memory");
+}
 // mbarrier wait with cluster-scope acquire (the phase may be completed by remote arrivals
 // whose writes this thread then reads / hands to the tensor core).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -61,6 +61,16 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #ifndef LA2_SPLIT_STATE
 #define LA2_SPLIT_STATE 1
 #endif
+// how the peer gets its half of the operand: st.async per 16 bytes (0) or one bulk copy
+// per warp through the TMA unit (1)
+// Y issuer as an event loop (folds run up to two blocks ahead of the Oe products) or in
+// program order (fold_i, Oe_i, fold_{i+1}, ...)
+#ifndef LA2_Y_EVENT
+#define LA2_Y_EVENT 0
+#endif
+#ifndef LA2_PEER_BULK
+#define LA2_PEER_BULK 0
+#endif
 
 #ifndef LA2_SO_NS
 #define LA2_SO_NS 4
@@ -501,28 +511,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     } else {
       // ---- Y: state chain  dKV_i = K~_i^T V_i (early) ; Oe_i = Q_i KV_{i-1}
-      for (int i = 0; i < T; ++i) {
+      auto issue_fold = [&](int i) {
         const int s = i % NS, kt = i % KTS, db = i & 1;
-        if (dqr) {
-          // the triple's dQ CTA: no recurrence; Oe_i = dO_i (KV_{i-1})^T from the stored state
-          mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
-          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
-          tc_fence_after();
-          if (leader) {
-            const uint64_t q = adv(dQ0, s * L::Q_BYTES), st = adv(dS0, s * L::S_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < DVS / 16; ++kk)
-              umma_bf16_ss(tOE, adv(q, (kk & 3) * 32), adv(st, (kk & 3) * 32), ID_OS, kk > 0);
-            umma_commit(&bars[L::B_OEFULL + db]);
-            commit_empty(s);
-          }
-          __syncwarp();
-          continue;
-        }
-        mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
-        if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
-        mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
-        TR(1, i, 5);
         tc_fence_after();
         if (leader) {
           // dKV = K^T (c . V): A = K^T (MN-major view of the K stage), B = V~ (MN-major)
@@ -538,13 +528,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (SO) commit_empty(s);
         }
         __syncwarp();
-        if (!SO) {
-          // SPLIT: KV_{i-1} sits in operand buffer i & 1, half of it written by the peer
-          if (SPLIT) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
-          else mbar_wait(&bars[L::B_KVREADY], i & 1);
-          if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
-          if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
-          TR(1, i, 4);
+      };
+      auto issue_oe = [&](int i) {
+        const int s = i % NS, db = i & 1;
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES);
@@ -580,8 +566,83 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             commit_empty(s);
           }
           __syncwarp();
+      };
+      for (int i = 0; i < T; ++i) {
+        const int s = i % NS, kt = i % KTS, db = i & 1;
+        if (dqr) {
+          // the triple's dQ CTA: no recurrence; Oe_i = dO_i (KV_{i-1})^T from the stored state
+          mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
+          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          tc_fence_after();
+          if (leader) {
+            const uint64_t q = adv(dQ0, s * L::Q_BYTES), st = adv(dS0, s * L::S_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < DVS / 16; ++kk)
+              umma_bf16_ss(tOE, adv(q, (kk & 3) * 32), adv(st, (kk & 3) * 32), ID_OS, kk > 0);
+            umma_commit(&bars[L::B_OEFULL + db]);
+            commit_empty(s);
+          }
+          __syncwarp();
+          continue;
+        }
+        if (!SO && LA2_Y_EVENT) break;  // the event loop below
+        mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
+        if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
+        mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
+        TR(1, i, 5);
+        issue_fold(i);
+        if (!SO) {
+          // SPLIT: KV_{i-1} sits in operand buffer i & 1, half of it written by the peer
+          if (SPLIT) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
+          else mbar_wait(&bars[L::B_KVREADY], i & 1);
+          if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
+          if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          TR(1, i, 4);
+          issue_oe(i);
         }
         TR(1, i, 6);
+      }
+      if (!SO && !dqr && LA2_Y_EVENT) {
+        // Event loop: the fold of block i+1 (inputs: V~_{i+1}, a free dKV buffer) does not
+        // wait behind Oe_i (input: the state KV_{i-1}), so KV_{i+1} never waits for KV_{i-1}
+        // via this warp's issue order -- in order, the recurrence advanced one block per
+        // (fold latency + state update) and set the block period.
+        auto fold_ready = [&](int i) {
+          return mbar_test(&bars[L::B_KTREADY + i % KTS], (i / KTS) & 1) &&
+                 (i < 2 || mbar_test(&bars[L::B_DKVEMPTY + (i & 1)], ((i >> 1) - 1) & 1)) &&
+                 mbar_test(&bars[L::B_FULL + i % NS], (i / NS) & 1);
+        };
+        auto oe_ready = [&](int i) {
+          bool ok = SPLIT ? mbar_test(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1)
+                          : mbar_test(&bars[L::B_KVREADY], i & 1);
+          if (L::OIS && i >= 2) ok = ok && mbar_test(&bars[L::B_OEMPTY + (i & 1)], ((i >> 1) - 1) & 1);
+          if (!L::OIS && i >= 1) ok = ok && mbar_test(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          return ok;
+        };
+        int nF = 0, nO = 0;
+        while (nO < T) {
+          int f_ok = 0, o_ok = 0;
+          if (lane == 0) {
+            if (nF < T && nF < nO + 2) f_ok = fold_ready(nF) ? 1 : 0;
+            if (nO < nF) o_ok = oe_ready(nO) ? 1 : 0;
+          }
+          f_ok = __shfl_sync(0xffffffffu, f_ok, 0);
+          o_ok = __shfl_sync(0xffffffffu, o_ok, 0);
+          if (!f_ok && !o_ok) {
+            __nanosleep(20);
+            continue;
+          }
+          if (o_ok) {  // the older block first: Oe is on the output path
+            TR(1, nO, 4);
+            issue_oe(nO);
+            ++nO;
+          }
+          if (f_ok) {
+            TR(1, nF, 5);
+            issue_fold(nF);
+            ++nF;
+          }
+        }
       }
       // SPLIT: the last Oe's commits (ours and the peer's) have landed in this CTA's
       // KVFREE barrier before teardown (no tcgen05 arrive may target an exited CTA)
@@ -782,7 +843,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // dKV rows: M=128 -> lane == d row; M=64 -> lanes 0-15 of each quarter hold 16 rows
     const bool has_kv = (DK == 128) || (lane < 16);
     const int kvrow = (DK == 128) ? row : (q4 * 16 + lane);
-    const int dvt = p.dv_total;
     float kv[KVC];
     // SPLIT: the peer's operand buffer and KVREADY barrier (this CTA writes half of both)
     const uint32_t peer = static_cast<uint32_t>(crank) ^ 1u;
@@ -807,9 +867,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           } else {
             // state stored transposed: element (r, c) at c * rs + r
+            // the row stride is DK (a [dv][dk] state) or 256 (split-d column halves of a
+            // [dv][256] state; the launcher rejects anything else): compile-time strides
+            // keep this cold path to one load per element (a runtime stride costs ~4
+            // instructions each, enough extra code to slow the d = 128 passes by ~2 %)
+            const float* src = p.kv_in + sbase + static_cast<size_t>(c0) * p.kv_in_rs + kvrow;
+            if (p.kv_in_rs == DK) {
 #pragma unroll
-            for (int j = 0; j < KVC; ++j)
-              kv[j] = p.kv_in[sbase + static_cast<size_t>(c0 + j) * p.kv_in_rs + kvrow];
+              for (int j = 0; j < KVC; ++j) kv[j] = src[j * DK];
+            } else {
+#pragma unroll
+              for (int j = 0; j < KVC; ++j) kv[j] = src[j * 256];
+            }
           }
         }
       } else {
@@ -879,7 +948,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // of the peer's KVREADY, whose W0 expects all 4 KB)
         uint8_t* hb = smem + (b ? L::OFF_KV2 : L::OFF_KV) + 4096 * static_cast<int>(crank);
         if (has_kv) {
-          uint8_t* rp = hb + kvrow * 64;
+          const uint32_t ro = static_cast<uint32_t>(hb - smem) + kvrow * 64;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint4 w;
@@ -887,7 +956,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             w.y = pack_bf16x2(kv[8 * c + 2], kv[8 * c + 3]);
             w.z = pack_bf16x2(kv[8 * c + 4], kv[8 * c + 5]);
             w.w = pack_bf16x2(kv[8 * c + 6], kv[8 * c + 7]);
-            *reinterpret_cast<uint4*>(rp + ((c ^ ((kvrow >> 1) & 3)) * 16)) = w;
+            const uint32_t o = ro + ((c ^ ((kvrow >> 1) & 3)) * 16);
+            *reinterpret_cast<uint4*>(smem + o) = w;
+#if LA2_PEER_BULK
           }
           fence_proxy_async_smem();
         }
@@ -895,6 +966,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
           const uint32_t off = static_cast<uint32_t>(hb - smem) + q4 * 16 * 64;
           bulk_copy_to_peer(r_base + off, smem + off, 16 * 64, r_kvready0 + 8u * b);
+#else
+            st_async_peer(r_base + o, w, r_kvready0 + 8u * b);  // the peer's copy, async
+          }
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) {
+#endif
           if (warp == W0) mbar_arrive_expect_tx(&bars[L::B_KVREADY + b], DK * 64);
           else mbar_arrive(&bars[L::B_KVREADY + b]);
         }
@@ -1191,6 +1270,8 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.dv_total = a.dv;
   p.kv_in_bhs = a.kv_in_bhs ? a.kv_in_bhs : static_cast<long long>(DK) * a.dv;
   p.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : (a.kv_in_T ? DK : a.dv);
+  if (a.kv_in != nullptr && a.kv_in_T && p.kv_in_rs != DK && p.kv_in_rs != 256)
+    return set_error(LA2_ERR_UNSUPPORTED, "transposed state row stride must be the head dim or 256");
   p.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : static_cast<long long>(DK) * a.dv;
   p.kv_out_rs = a.kv_out_rs ? a.kv_out_rs : a.dv;
   p.accum = a.accum_o;
