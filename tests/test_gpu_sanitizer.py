@@ -1,5 +1,5 @@
 """compute-sanitizer over one small fwd+bwd step of the tcgen05 kernels (memcheck,
-racecheck, synccheck, initcheck): no out-of-bounds / uninitialised global accesses, no
+racecheck, synccheck, initcheck), replay and stored-state backward: no out-of-bounds / uninitialised global accesses, no
 shared-memory hazards, no illegal barrier use."""
 import os
 import shutil
@@ -22,6 +22,12 @@ pytestmark = pytest.mark.gpu
     ("racecheck", "1,3,700,64"),
     ("synccheck", "1,3,700,64"),
     ("initcheck", "1,3,700,128"),
+    # the d = 64 stored-state triple (forward storing the states, shared dK/dV recurrence
+    # with st.async operand exchange, stateless dQ CTA), also across persistent ranges
+    ("memcheck", "1,3,700,64,s"),
+    ("memcheck", "4,40,1000,64,s"),
+    ("racecheck", "1,3,700,64,s"),
+    ("synccheck", "1,3,700,64,s"),
 ])
 def test_sanitizer_clean(tool, shape):
     if not os.path.exists(SAN):

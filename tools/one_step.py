@@ -1,13 +1,22 @@
-"""One forward + one backward at a given shape (for ncu captures)."""
+"""One forward + one backward at a given shape "B,H,N,d[,s]" (for ncu / compute-sanitizer);
+",s" runs the stored-state pair la2_forward_states + la2_backward_states (the d = 64 dQ/dK/dV
+triple) instead of la2_forward + la2_backward."""
 import sys
 sys.path.insert(0, '.')
 import torch
 import paper_2401_04658_b200 as la2
 from bench import alibi_decay
-B, H, N, D = (tuple(map(int, sys.argv[1].split(','))) if len(sys.argv) > 1 else (8, 16, 16384, 64))
+from paper_2401_04658_b200 import ops
+spec = sys.argv[1].split(',') if len(sys.argv) > 1 else ['8', '16', '16384', '64']
+B, H, N, D = map(int, spec[:4])
+stored = len(spec) > 4 and spec[4] == 's'
 dev = torch.device('cuda', 0)
 q, k, v, do = ((torch.rand(B, H, N, D, device=dev) * 2 - 1).bfloat16() for _ in range(4))
 dec = la2.decay_tensor(alibi_decay(H), H, dev)
-la2.la2_forward(q, k, v, dec)
-la2.la2_backward(q, k, v, do, dec)
+if stored:
+    _, _, blocks = ops.la2_forward_states(q, k, v, dec)
+    ops.la2_backward_states(q, k, v, do, dec, blocks)
+else:
+    la2.la2_forward(q, k, v, dec)
+    la2.la2_backward(q, k, v, do, dec)
 torch.cuda.synchronize()
