@@ -63,6 +63,11 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #endif
 // how the peer gets its half of the operand: st.async per 16 bytes (0) or one bulk copy
 // per warp through the TMA unit (1)
+// d = 64 with O in the upper half of its S buffer too (O and Oe double-buffered; S reuse
+// then waits for the epilogue instead of PV)
+#ifndef LA2_OIS64
+#define LA2_OIS64 0
+#endif
 // Y issuer as an event loop (folds run up to two blocks ahead of the Oe products) or in
 // program order (fold_i, Oe_i, fold_{i+1}, ...)
 #ifndef LA2_Y_EVENT
@@ -111,7 +116,7 @@ struct TcLayout {
   // dKV[2] @384,448. Otherwise (d = 64): S[2] @0,128 (P in cols +0..31, +64..95) | O @256
   // | Oe @320 | dKV[2] @384,448 -- S_{i+2} then only waits for PV_i, not for the epilogue.
   // State-only: dKV[2] @0,64.
-  static constexpr bool OIS = (DK == 128);
+  static constexpr bool OIS = (DK == 128) || (LA2_OIS64 != 0);
   // d = 128 (full passes): the V~ copy runs on its own warp, overlapping the state update
   // (-10 % at C3). d = 64 keeps it in the state warps: there the kernel is close to
   // issue-bound and a 16th busy warp slows its sub-partition (+8 %). State-only passes
@@ -545,13 +550,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const uint64_t dm = sdesc_sw64(kvb, 4096, 512);
 #pragma unroll
                 for (int kk = 0; kk < DK / 16; ++kk)
-                  umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32), adv(dm, kk * 1024), ID_O,
-                               kk > 0);
+                  umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
+                               adv(dm, kk * 1024), ID_O, kk > 0);
               } else {
                 const uint64_t dk = sdesc_sw64(kvb, 16, 512);
 #pragma unroll
                 for (int kk = 0; kk < DK / 16; ++kk)
-                  umma_bf16_ss(tOE, adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
+                  umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
                                adv(dk, (kk >> 1) * 4096 + (kk & 1) * 32), ID_OS, kk > 0);
               }
             } else {
@@ -572,13 +577,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (dqr) {
           // the triple's dQ CTA: no recurrence; Oe_i = dO_i (KV_{i-1})^T from the stored state
           mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);
-          if (i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
+          if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES), st = adv(dS0, s * L::S_BYTES);
 #pragma unroll
             for (int kk = 0; kk < DVS / 16; ++kk)
-              umma_bf16_ss(tOE, adv(q, (kk & 3) * 32), adv(st, (kk & 3) * 32), ID_OS, kk > 0);
+              umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk & 3) * 32), adv(st, (kk & 3) * 32), ID_OS,
+                           kk > 0);
             umma_commit(&bars[L::B_OEFULL + db]);
             commit_empty(s);
           }
