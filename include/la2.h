@@ -184,6 +184,34 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
                     float* state, void* o, int B, int H, int d, int dv, int dtype, void* stream);
 
 /*
+ * Double precision: the reference's default dtype (every tila routine computes in the
+ * input dtype, np.result_type; pkg/src/tila/reference.py:54-74). fp64 storage and
+ * arithmetic on the CUDA cores (DFMA), decay powers by iterated products flushed below
+ * the smallest normal double (tila.power_table, reference.py:75-100). All tensors,
+ * decay and states are double; shapes and semantics as the single-precision calls:
+ *   la2_forward_f64      tila.tiled_forward / chunked_forward  (kernel.py:122-162)
+ *   la2_backward_f64     tila.tiled_backward                  (kernel.py:165-233)
+ *   la2_decode_step_f64  tila.inference_step                  (reference.py:162-181)
+ *   la2_check_decay_f64  the decay validation of reference.py:42-44
+ * d, dv <= 256; no sequence split, no tensor cores: a correctness path for the tila
+ * adapter (the reference's 1e-10 gates), not a throughput path. `block` is the
+ * reference's block argument: the kernels tile by it when it is <= 16 (or when it covers
+ * a sequence of <= 16 tokens: one tile), else by its largest divisor <= 16 (0: 16), so
+ * results are deterministic per block and chunk boundaries aligned to it give bitwise the
+ * one-call result, as in the reference.
+ */
+LA2_API int la2_forward_f64(const double* q, const double* k, const double* v, const double* decay,
+                            double* o, const double* kv_in, double* kv_out, int B, int H, int N,
+                            int d, int dv, int block, void* stream);
+LA2_API int la2_backward_f64(const double* q, const double* k, const double* v, const double* dout,
+                             const double* decay, double* dq, double* dk, double* dv,
+                             const double* kv_in, const double* dkv_in, double* dkv_out, int B, int H,
+                             int N, int d, int dv_dim, int block, void* stream);
+LA2_API int la2_decode_step_f64(const double* q, const double* k, const double* v, const double* decay,
+                                double* state, double* o, int B, int H, int d, int dv, void* stream);
+LA2_API int la2_check_decay_f64(const double* decay, int H, void* stream);
+
+/*
  * Scheduling knobs of the tensor-core kernels (process-wide; not a reference
  * interface). Results do not depend on them: the persistent schedule hands the fp32
  * state between work ranges exactly, so outputs are bitwise identical either way.

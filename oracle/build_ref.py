@@ -17,6 +17,7 @@ import shutil
 from pathlib import Path
 
 REF_PKG = Path("/root/reference/pkg/src/tila")
+REF_TESTS = Path("/root/reference/pkg/tests")
 OUT = Path(__file__).resolve().parent / "_ref"
 
 
@@ -30,6 +31,11 @@ def build(out: Path = OUT) -> Path | None:
     out.mkdir(parents=True, exist_ok=True)
     shutil.copytree(REF_PKG, dst, dirs_exist_ok=True,
                     ignore=shutil.ignore_patterns("__pycache__", "*.pyc"))
+    # the reference's own test suite, run against the GPU adapter by
+    # tests/test_gpu_reference_suites.py (tests/ref_gpu_plugin.py patches the kernels in)
+    if REF_TESTS.is_dir():
+        shutil.copytree(REF_TESTS, out / "tests", dirs_exist_ok=True,
+                        ignore=shutil.ignore_patterns("__pycache__", "*.pyc"))
     return dst
 
 

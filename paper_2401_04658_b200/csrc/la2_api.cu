@@ -590,6 +590,84 @@ int la2_check_decay(const float* decay, int H, void* stream) {
   return 0;
 }
 
+// ---------------------------------------------------------------- fp64 (la2_f64.cu)
+static int check_f64(int B, int H, int N, int d, int dv, const double* decay) {
+  if (B < 1 || H < 1) return set_error(LA2_ERR_VALUE, "B and H must be >= 1");
+  if (N < 1) return set_error(LA2_ERR_VALUE, "sequence length N must be >= 1");
+  if (d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "d and dv must be >= 1");
+  if (d > 256 || dv > 256) return set_error(LA2_ERR_UNSUPPORTED, "fp64 path supports d, dv <= 256");
+  if (decay == nullptr) return set_error(LA2_ERR_VALUE, "decay pointer is null");
+  return 0;
+}
+
+int la2_forward_f64(const double* q, const double* k, const double* v, const double* decay, double* o,
+                    const double* kv_in, double* kv_out, int B, int H, int N, int d, int dv, int block,
+                    void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_f64(B, H, N, d, dv, decay)) return rc;
+  if (!q || !k || !v || !o) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  return launch_f64(q, k, v, o, decay, kv_in, 0, kv_out, B, H, N, d, dv, 0, block,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// The backward as three F passes, exactly like la2_backward's SIMT path:
+// dQ = F(dO, V, K) (state KV^T), dK = F_rev(V, dO, Q) (state dKV^T), dV = F_rev(K, Q, dO).
+int la2_backward_f64(const double* q, const double* k, const double* v, const double* dout,
+                     const double* decay, double* dq, double* dk, double* dv, const double* kv_in,
+                     const double* dkv_in, double* dkv_out, int B, int H, int N, int d, int dvd, int block,
+                     void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_f64(B, H, N, d, dvd, decay)) return rc;
+  if (!q || !k || !v || !dout || !dq || !dk || !dv) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, q)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_f64(dout, v, k, dq, decay, kv_in, 1, nullptr, B, H, N, dvd, d, 0, block, st)) return rc;
+  if (int rc = launch_f64(v, dout, q, dk, decay, dkv_in, 1, nullptr, B, H, N, dvd, d, 1, block, st)) return rc;
+  return launch_f64(k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, 1, block, st);
+}
+
+int la2_decode_step_f64(const double* q, const double* k, const double* v, const double* decay,
+                        double* state, double* o, int B, int H, int d, int dv, void* stream) {
+  g_err[0] = 0;
+  if (B < 1 || H < 1 || d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad decode shape");
+  if (!q || !k || !v || !decay || !state || !o) return set_error(LA2_ERR_VALUE, "null pointer");
+  if (int rc = bind_device(stream, state)) return rc;
+  return launch_decode_f64(q, k, v, decay, state, o, B, H, d, dv, static_cast<cudaStream_t>(stream));
+}
+
+int la2_check_decay_f64(const double* decay, int H, void* stream) {
+  g_err[0] = 0;
+  if (decay == nullptr) return set_error(LA2_ERR_VALUE, "decay pointer is null");
+  if (H < 1) return set_error(LA2_ERR_VALUE, "H must be >= 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<double> h(static_cast<size_t>(H));
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, decay) != cudaSuccess) cudaGetLastError();
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (int rc = bind_device(stream, decay)) return rc;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return set_error(LA2_ERR_UNSUPPORTED,
+                       "la2_check_decay_f64 synchronizes the stream: call it before graph capture");
+    }
+    cudaError_t e = cudaMemcpyAsync(h.data(), decay, H * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_cuda_error("la2_check_decay_f64", e);
+  } else {
+    std::memcpy(h.data(), decay, H * sizeof(double));
+  }
+  for (int i = 0; i < H; ++i) {
+    if (!(h[i] > 0.0 && h[i] <= 1.0)) {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "decay rate must be in (0, 1], got %g (head %d)", h[i], i);
+      return set_error(LA2_ERR_VALUE, buf);
+    }
+  }
+  return 0;
+}
+
 int la2_decode_step(const void* q, const void* k, const void* v, const float* decay, float* state,
                     void* o, int B, int H, int d, int dv, int dtype, void* stream) {
   g_err[0] = 0;

@@ -85,6 +85,13 @@ int tma_encoder_ready();
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows, long long head_stride = 0,
                    long long row_pitch = 0);
 int launch_simt(const FArgs& a, cudaStream_t st);
+// fp64 F pass (la2_f64.cu): one launch of the block recurrence (reverse = F_rev) and
+// the fp64 decode step
+int launch_f64(const double* q, const double* k, const double* v, double* o, const double* decay,
+               const double* kv_in, int kv_in_T, double* kv_out, int B, int H, int N, int dk, int dv,
+               int reverse, int block, cudaStream_t st);
+int launch_decode_f64(const double* q, const double* k, const double* v, const double* decay,
+                      double* state, double* o, int B, int H, int d, int dv, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);
 int launch_state_scan(const float* chunk_states, const float* decay, const float* init,

@@ -24,14 +24,18 @@ from . import _lib
 
 DecayLike = Union[float, Sequence[float], torch.Tensor]
 
-_DTYPE_CODE = {torch.bfloat16: _lib.LA2_BF16, torch.float32: _lib.LA2_FP32}
+# float64 runs the double-precision entry points (la2_*_f64, include/la2.h): the reference's
+# default dtype, computed in fp64 as the reference does (no narrowing to fp32)
+_DTYPE_CODE = {torch.bfloat16: _lib.LA2_BF16, torch.float32: _lib.LA2_FP32, torch.float64: -64}
+_F64 = torch.float64
 
 
 def _code(t: torch.Tensor) -> int:
     try:
         return _DTYPE_CODE[t.dtype]
     except KeyError:
-        raise ValueError(f"unsupported dtype {t.dtype}; expected torch.bfloat16 or torch.float32") from None
+        raise ValueError(f"unsupported dtype {t.dtype}; expected torch.bfloat16, torch.float32 or "
+                         "torch.float64") from None
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -45,7 +49,7 @@ def _stream(dev: torch.device) -> int:
                                               torch.cuda.current_device())
 
 
-def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
+def decay_tensor(decay: DecayLike, H: int, device: torch.device, dtype=torch.float32) -> torch.Tensor:
     """Per-head decay as a contiguous float32 [H] tensor on ``device``.
 
     Values are validated with the reference's rule lam in (0, 1]
@@ -57,11 +61,11 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
     into NaN outputs, never plausible numbers).
     """
     if isinstance(decay, torch.Tensor) and decay.is_cuda:
-        if (decay.dtype == torch.float32 and decay.dim() == 1 and decay.numel() == H
+        if (decay.dtype == dtype and decay.dim() == 1 and decay.numel() == H
                 and decay.device == device and decay.is_contiguous()):
             _check_cuda_decay(decay)
             return decay  # fast path: already a prepared per-head decay vector
-        d = decay.to(device=device, dtype=torch.float32).reshape(-1)
+        d = decay.to(device=device, dtype=dtype).reshape(-1)
         if d.numel() == 1:
             d = d.expand(H)
         if d.numel() != H:
@@ -82,7 +86,7 @@ def decay_tensor(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor
     for lam in vals:
         if not (0.0 < lam <= 1.0):
             raise ValueError(f"decay rate must be in (0, 1], got {lam}")
-    return torch.tensor(vals, dtype=torch.float32, device=device)
+    return torch.tensor(vals, dtype=dtype, device=device)
 
 
 _DECAY_CACHE: dict = {}
@@ -104,29 +108,30 @@ def _check_cuda_decay(d: torch.Tensor, src: Optional[torch.Tensor] = None) -> No
         return
     if torch.cuda.is_current_stream_capturing():
         return  # cannot synchronize inside capture; the kernels poison invalid lam with NaN
-    _lib.call("la2_check_decay", d.data_ptr(), d.numel(), _stream(d.device))
+    _lib.call("la2_check_decay_f64" if d.dtype == _F64 else "la2_check_decay", d.data_ptr(), d.numel(),
+              _stream(d.device))
     if len(_CHECKED) >= 4096:
         for key in [k for k, (r, _) in _CHECKED.items() if r() is None]:
             del _CHECKED[key]
     _CHECKED[id(owner)] = (weakref.ref(owner), stamp)
 
 
-def _decay(decay: DecayLike, H: int, device: torch.device) -> torch.Tensor:
+def _decay(decay: DecayLike, H: int, device: torch.device, dtype=torch.float32) -> torch.Tensor:
     """decay_tensor for the ops' own use: host values (lists, floats, CPU tensors) are
     validated and uploaded once per distinct (values, device) and the device copy is
     reused -- a fresh upload costs ~16 us of host time per call. The cached tensor is
     never handed to the caller (only read by the kernels)."""
     if isinstance(decay, torch.Tensor) and decay.is_cuda:
-        return decay_tensor(decay, H, device)
+        return decay_tensor(decay, H, device, dtype)
     if isinstance(decay, (int, float)):
-        key = ((float(decay),), H, device)
+        key = ((float(decay),), H, device, dtype)
     elif isinstance(decay, torch.Tensor):
-        key = (tuple(decay.detach().double().reshape(-1).tolist()), H, device)
+        key = (tuple(decay.detach().double().reshape(-1).tolist()), H, device, dtype)
     else:
-        key = (tuple(float(x) for x in decay), H, device)
+        key = (tuple(float(x) for x in decay), H, device, dtype)
     t = _DECAY_CACHE.get(key)
     if t is None:
-        t = decay_tensor(list(key[0]), H, device)
+        t = decay_tensor(list(key[0]), H, device, dtype)
         if len(_DECAY_CACHE) >= 256:
             _DECAY_CACHE.clear()
         _DECAY_CACHE[key] = t
@@ -156,12 +161,12 @@ def _check_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     return B, H, N, d, v.shape[3]
 
 
-def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name) -> Optional[torch.Tensor]:
+def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name, dtype=torch.float32) -> Optional[torch.Tensor]:
     if t is None:
         return None
     if tuple(t.shape) != (B, H, d, dv):
         raise ValueError(f"{name} must have shape {(B, H, d, dv)}, got {tuple(t.shape)}")
-    return t.to(device=device, dtype=torch.float32).contiguous()
+    return t.to(device=device, dtype=dtype).contiguous()
 
 
 # ------------------------------------------------------ intra-GPU sequence split
@@ -184,6 +189,8 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
     (the state scan's limit). Measured on B200 (tools/fp32_split.py): C1 fp32 fwd+bwd
     1.22 ms at 8 chunks -> 0.53 ms at 64.
     """
+    if dtype == torch.float64:
+        return 1  # the fp64 correctness path runs unsplit
     units = B * H * ((dv + 63) // 64)
     g = 1
     if dtype == torch.bfloat16 and d in TC_DIMS and dv % 64 == 0 and dv <= 256:
@@ -252,13 +259,24 @@ def split_backward(q, k, v, d_out, decay, g: int, prefix, dkv_in=None, output_dk
 
 # ------------------------------------------------------------------ raw passes
 def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
-                output_final_state: bool = False):
+                output_final_state: bool = False, block: int = 0):
     """One forward pass. Returns ``(o, kv_out)``; kv_out is None unless requested.
 
-    kv_in (fp32 ``[B,H,d,dv]``) is the carried state of tila.chunked_forward
-    (pkg/src/tila/kernel.py:142-162); kv_out its returned KvState.kv.
+    kv_in (fp32 ``[B,H,d,dv]``, fp64 for fp64 inputs) is the carried state of
+    tila.chunked_forward (pkg/src/tila/kernel.py:142-162); kv_out its returned KvState.kv.
+    ``block`` (fp64 only) is the reference's block argument: the fp64 kernels tile by it
+    (see include/la2.h la2_forward_f64); the bf16 / fp32 kernels choose their own tile.
     """
     B, H, N, d, dv = _check_qkv(q, k, v)
+    if q.dtype == _F64:
+        dec = _decay(decay, H, q.device, _F64)
+        kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in", _F64)
+        kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=_F64) if output_final_state else None
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        o = torch.empty_like(v)
+        _lib.call("la2_forward_f64", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in), _ptr(kv_out),
+                  B, H, N, d, dv, int(block), _stream(q.device))
+        return o, kv_out
     dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
@@ -349,7 +367,8 @@ def _head_stride(t: torch.Tensor) -> Optional[int]:
     return ld
 
 
-def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, output_dkv: bool = False):
+def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, output_dkv: bool = False,
+                 block: int = 0):
     """Gradients of sum(d_out * O) (tila.tiled_backward, pkg/src/tila/kernel.py:165-233).
 
     Returns ``(dq, dk, dv, dkv_out)``. dkv_in is the mirrored state from tokens
@@ -360,6 +379,17 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     B, H, N, d, dv = _check_qkv(q, k, v)
     if d_out.shape != v.shape or d_out.dtype != v.dtype:
         raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
+    if q.dtype == _F64:
+        dec = _decay(decay, H, q.device, _F64)
+        kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in", _F64)
+        dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in", _F64)
+        dkv_out = torch.empty(B, H, d, dv, device=q.device, dtype=_F64) if output_dkv else None
+        q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous()
+        dq, dk, dvv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        _lib.call("la2_backward_f64", _ptr(q), _ptr(k), _ptr(v), _ptr(d_out), _ptr(dec), _ptr(dq), _ptr(dk),
+                  _ptr(dvv), _ptr(kv_in), _ptr(dkv_in), _ptr(dkv_out), B, H, N, d, dv, int(block),
+                  _stream(q.device))
+        return dq, dk, dvv, dkv_out
     dec = _decay(decay, H, q.device)
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     dkv_in = _state(dkv_in, B, H, d, dv, q.device, "dkv_in")
@@ -460,7 +490,8 @@ def state_scan(states: torch.Tensor, decay: DecayLike, lens: Sequence[int],
 
 
 def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.Tensor:
-    """One recurrent decode step, in place on ``state`` (fp32 ``[B,H,d,dv]``).
+    """One recurrent decode step, in place on ``state`` (fp32 ``[B,H,d,dv]``; float64 for
+    float64 inputs).
 
     state <- lam*state + k_t^T v_t; returns o_t = q_t state
     (tila.inference_step, pkg/src/tila/reference.py:162-181).
@@ -470,11 +501,18 @@ def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.T
         raise ValueError("decode_step expects q_t, k_t [B,H,d] and v_t [B,H,dv]")
     B, H, d = q_t.shape
     dv = v_t.shape[2]
-    if tuple(state.shape) != (B, H, d, dv) or state.dtype != torch.float32 or not state.is_contiguous():
-        raise ValueError(f"state must be a contiguous float32 tensor of shape {(B, H, d, dv)}")
+    sdt = _F64 if q_t.dtype == _F64 else torch.float32
+    if tuple(state.shape) != (B, H, d, dv) or state.dtype != sdt or not state.is_contiguous():
+        raise ValueError(f"state must be a contiguous {sdt} tensor of shape {(B, H, d, dv)}")
     if not (q_t.dtype == k_t.dtype == v_t.dtype):
         raise ValueError("q_t, k_t, v_t must share a dtype")
     q_t, k_t, v_t = q_t.contiguous(), k_t.contiguous(), v_t.contiguous()
+    if q_t.dtype == _F64:
+        dec = _decay(decay, H, q_t.device, _F64)
+        o = torch.empty_like(v_t)
+        _lib.call("la2_decode_step_f64", _ptr(q_t), _ptr(k_t), _ptr(v_t), _ptr(dec), _ptr(state), _ptr(o),
+                  B, H, d, dv, _stream(q_t.device))
+        return o
     dec = _decay(decay, H, q_t.device)
     o = torch.empty_like(v_t)
     _lib.call("la2_decode_step", _ptr(q_t), _ptr(k_t), _ptr(v_t), _ptr(dec), _ptr(state), _ptr(o),
@@ -548,7 +586,8 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
     """Causal linear attention with per-head exponential decay, on the GPU.
 
     Args:
-      q, k: ``[B, H, N, d]``; v: ``[B, H, N, dv]`` CUDA tensors, bf16 or fp32.
+      q, k: ``[B, H, N, d]``; v: ``[B, H, N, dv]`` CUDA tensors, bf16, fp32 or fp64 (fp64:
+        the double-precision CUDA-core path, states in fp64 too).
       decay: per-head lambda in (0, 1] -- float, sequence of H floats or a tensor.
       initial_state: optional fp32 ``[B, H, d, dv]`` state carried in.
       output_final_state: also return the fp32 final state.
@@ -557,11 +596,12 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
     Returns ``o`` (``[B,H,N,dv]``, input dtype), or ``(o, final_state)``.
     """
     _check_qkv(q, k, v)
-    dec = _decay(decay, q.shape[1], q.device)
+    sdt = _F64 if q.dtype == _F64 else torch.float32  # state / decay precision
+    dec = _decay(decay, q.shape[1], q.device, sdt)
     if initial_state is not None:
         B, H, N, d = q.shape
         if tuple(initial_state.shape) != (B, H, d, v.shape[3]):
             raise ValueError(f"initial_state must have shape {(B, H, d, v.shape[3])}")
-        if initial_state.dtype != torch.float32:
-            initial_state = initial_state.float()
+        if initial_state.dtype != sdt:
+            initial_state = initial_state.to(sdt)
     return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state), seq_split)

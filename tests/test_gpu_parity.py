@@ -995,3 +995,74 @@ def test_autograd_uses_stored_states():
     rq, rk, rv = port.bhnd_backward(Q, K, V, DO, [0.999] * 4)
     errs = {"o": rel(o, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
     assert max(errs.values()) <= BF16_TOL, errs
+
+
+# ------------------------------------------------------------------ fp64 path
+FP64_TOL = 1e-12  # the reference's own fp64 gates are 1e-10 .. 1e-12 (pkg/tests/test_kernel.py)
+
+
+@pytest.mark.parametrize("B,H,N,d,dv", [(1, 8, 300, 64, 64), (2, 3, 517, 4, 7), (1, 2, 96, 128, 256),
+                                        (1, 1, 1, 1, 1)])
+def test_fp64_forward_backward_against_oracle(B, H, N, d, dv):
+    """float64 inputs run the double-precision kernels (la2_*_f64): the reference's
+    default dtype, computed in fp64 like the reference -- agreement to ~1e-15."""
+    decay = C1_DECAY[:H] if H <= 8 else [0.9] * H
+    q, k, v, do = inputs(B, H, N, d, dv, torch.float64, seed=N)
+    Q, K, V, DO = (t.numpy() for t in (q, k, v, do))
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    o = la2.lightning_attn2(qg, kg, vg, decay)
+    assert o.dtype == torch.float64
+    o.backward(do.to(DEV))
+    ro = port.bhnd_oracle_forward(Q, K, V, decay)
+    rq, rk, rv = port.bhnd_oracle_backward(Q, K, V, DO, decay)
+    for got, ref in ((o, ro), (qg.grad, rq), (kg.grad, rk), (vg.grad, rv)):
+        assert rel(got, ref) <= FP64_TOL
+
+
+def test_fp64_carried_states_and_decode():
+    """Chunked fp64 forward with carried fp64 state, the backward's dkv_out, and the fp64
+    decode step against the port (tila.chunked_forward / inference_step)."""
+    B, H, N, d, dv = 1, 3, 200, 16, 24
+    decay = [0.5, 0.999, 1.0]
+    q, k, v, do = inputs(B, H, N, d, dv, torch.float64, seed=5)
+    Q, K, V = (t.numpy() for t in (q, k, v))
+    kv0 = np.random.default_rng(3).uniform(-1, 1, (B, H, d, dv))
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, kv_in=torch.from_numpy(kv0).to(DEV), output_final_state=True)
+    assert o.dtype == torch.float64 and kv.dtype == torch.float64
+    ro, rkv = port.bhnd_forward(Q, K, V, decay, block=16, kv_in=kv0)
+    assert rel(o, ro) <= FP64_TOL and rel(kv, rkv) <= FP64_TOL
+    # decode: one token absorbed into the final state
+    st = kv.clone()
+    qt, kt, vt = (rand((B, H, c), 90 + i, torch.float64) for i, c in enumerate((d, d, dv)))
+    ot = la2.decode_step(*gpu(qt, kt, vt), decay, st)
+    for h in range(H):
+        ro_t, rs = port.inference_step(qt[0, h].numpy(), kt[0, h].numpy(), vt[0, h].numpy(),
+                                       port.KvState(rkv[0, h].copy()), decay[h])
+        assert port.rel_err(to64(ot[0, h]), ro_t) <= FP64_TOL
+        assert port.rel_err(to64(st[0, h]), rs.kv) <= FP64_TOL
+
+
+def test_tila_api_fp64_matches_reference_precision():
+    """The adapter keeps float64 in float64: the reference's fp64 tolerances hold
+    (pkg/tests/test_kernel.py:85-95 seeded-against-oracle at 1e-11)."""
+    q, k, v, d_out = port.case_inputs(64, 8, 8, 2)
+    res = tila_api.tiled_forward(q, k, v, 0.9, 16)
+    assert res.o.dtype == np.float64
+    assert port.rel_err(res.o, port.oracle_forward(q, k, v, 0.9)) <= 1e-11
+    g = tila_api.tiled_backward(q, k, v, d_out, 0.9, 16)
+    go = port.oracle_backward(q, k, v, d_out, 0.9)
+    for a in ("dq", "dk", "dv"):
+        assert port.rel_err(getattr(g, a), getattr(go, a)) <= 1e-11
+    # single precision stays single precision (the fp32 kernels)
+    q32, k32, v32 = (x.astype(np.float32) for x in (q, k, v))
+    res32 = tila_api.tiled_forward(q32, k32, v32, 0.9, 8)
+    assert res32.o.dtype == np.float32
+    assert port.rel_err(res32.o.astype(np.float64), port.oracle_forward(q, k, v, 0.9)) <= FP32_TOL
+
+
+def test_fp64_invalid_decay_raises():
+    q, k, v, _ = inputs(1, 2, 8, 4, 4, torch.float64)
+    with pytest.raises(ValueError):
+        la2.lightning_attn2(*gpu(q, k, v), [0.5, 1.5])
+    with pytest.raises(ValueError):
+        la2.lightning_attn2(*gpu(q, k, v), torch.tensor([0.5, 0.0], dtype=torch.float64, device=DEV))
