@@ -19,7 +19,8 @@
  *   v, o, dout, dv        [B, H, N, dv]
  *   decay                 [H] float32, lambda_h in (0, 1]   (per-head decay)
  *   states (kv, dkv)      [B, H, d, dv] float32
- * Element type of q/k/v/o/... is selected by `dtype` (LA2_BF16 or LA2_FP32).
+ * Element type of q/k/v/o/... is selected by `dtype` (LA2_BF16 or LA2_FP32); float64
+ * (the reference's default dtype) has its own entry points, la2_*_f64, below.
  *
  * Kernel selection is a pure function of (dtype, d, dv):
  *   bf16, d in {64,128,256}, dv % 64 == 0 -> tcgen05/TMA tensor-core kernel (d = 256:
