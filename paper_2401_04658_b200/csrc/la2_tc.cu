@@ -68,6 +68,16 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #ifndef LA2_OIS64
 #define LA2_OIS64 0
 #endif
+// d = 64 in-order X issuer: probe whether block i+1 has landed before issuing S_{i+1}, and
+// issue PV_i first if it has not
+#ifndef LA2_X_OPPORTUNISTIC
+#define LA2_X_OPPORTUNISTIC 0
+#endif
+// X issuer at d = 64 as the event loop too (S_{i+1} and PV_i issued as each becomes
+// ready) instead of the in-order S_{i+1}, PV_i, which makes PV_i wait for block i+1 to land
+#ifndef LA2_X_EVENT64
+#define LA2_X_EVENT64 0
+#endif
 // Y issuer as an event loop (folds run up to two blocks ahead of the Oe products) or in
 // program order (fold_i, Oe_i, fold_{i+1}, ...)
 #ifndef LA2_Y_EVENT
@@ -417,13 +427,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // and the O accumulator free) are issued as soon as each is ready, so PV_i never
       // waits behind the arrival of block i+1 -- that coupling would keep only one stage
       // load in flight with a 2-stage ring. S runs at most one block ahead of PV.
-      if (!SO && NS >= 3) {
+      if (!SO && NS >= 3 && !LA2_X_EVENT64) {
         // deep ring (d = 64): block i+1 has normally landed before PV_i is due, so the
         // plain order S_{i+1}, PV_i keeps the tensor pipe fed with the least polling
-        auto issue_S = [&](int j) {
+        auto issue_S = [&](int j, bool ready = false) {
           const int s = j % NS, b = j & 1;
-          mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
-          if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
+          if (!ready) {
+            mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+            if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
+          }
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
@@ -441,7 +453,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int s = i % NS, b = i & 1;
           const uint64_t v = adv(dV0, s * L::V_BYTES);
           TR(1, i, 0);
-          if (i + 1 < T) issue_S(i + 1);
+          // S_{i+1} first when block i+1 has landed; otherwise PV_i first (one probe, no
+          // spinning), so PV_i -- and the stage release behind it -- never waits for a load
+          bool s_next = (i + 1 >= T);
+          if (!s_next && LA2_X_OPPORTUNISTIC && !REV) {  // forward scans only: measured faster
+                                                          // there, slower for the reverse pair / triple
+            int ok = 0;
+            if (lane == 0)
+              ok = mbar_test(&bars[L::B_FULL + (i + 1) % NS], ((i + 1) / NS) & 1) &&
+                   (i + 1 < 2 || mbar_test(&bars[L::B_SFREE + ((i + 1) & 1)], (((i + 1) >> 1) - 1) & 1));
+            if (__shfl_sync(0xffffffffu, ok, 0)) {
+              issue_S(i + 1, true);
+              s_next = true;
+            }
+          } else if (!s_next) {
+            issue_S(i + 1);
+            s_next = true;
+          }
           TR(1, i, 1);
           mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
           TR(1, i, 2);
@@ -460,6 +488,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             commit_empty(s);
           }
           __syncwarp();
+          if (!s_next) issue_S(i + 1);
         }
       } else if (!SO) {
         int nS = 0, nP = 0;
