@@ -23,9 +23,12 @@
  * (the reference's default dtype) has its own entry points, la2_*_f64, below.
  *
  * Kernel selection is a pure function of (dtype, d, dv):
- *   bf16, d in {64,128,256}, dv % 64 == 0 -> tcgen05/TMA tensor-core kernel (d = 256:
- *                                           split-d, two 128-wide passes, the second
- *                                           adding into o by TMA reduce-add)
+ *   bf16, d and dv multiples of 8 up to 256 -> tcgen05/TMA tensor-core kernel: d <= 64 /
+ *                                           <= 128 on the 64- / 128-wide kernel, narrower
+ *                                           operands zero-filled by the TMA unit; d > 128
+ *                                           split-d (two passes over the column halves, the
+ *                                           second adding into o by TMA reduce-add); dv in
+ *                                           64-wide value slices, the last one partial
  *   otherwise, d <= 256 and dv <= 256   -> SIMT fp32-accumulate kernel
  *   anything else                       -> LA2_ERR_UNSUPPORTED (no fallback)
  *

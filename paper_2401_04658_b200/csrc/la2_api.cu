@@ -165,9 +165,11 @@ static int join_side(SideStream* side, cudaStream_t st) {
   return 0;
 }
 
+// bf16 widths that are multiples of 8 (16-byte TMA row pitch) up to 256 run on the tensor
+// cores: d <= 64 / <= 128 on the DK = 64 / 128 kernel (narrower operands zero-padded by the
+// TMA unit), d in (128, 256] as split-d; dv in 64-wide value slices, the last one partial.
 static bool tc_eligible(int dtype, int dk, int dv) {
-  return dtype == LA2_BF16 && (dk == 64 || dk == 128 || dk == 256) && dv % 64 == 0 && dv >= 64 &&
-         dv <= 256;
+  return dtype == LA2_BF16 && dk >= 8 && dk <= 256 && dk % 8 == 0 && dv >= 8 && dv <= 256 && dv % 8 == 0;
 }
 
 // Split-d: an F pass with a 256-wide q/k is the sum of two 128-wide passes over the column
@@ -182,7 +184,7 @@ static int run_f_split_d(const FArgs& a, cudaStream_t st) {
   const long long dk = a.dk, dv = a.dv;
   for (int h = 0; h < 2; ++h) {
     FArgs b = a;
-    b.dk = 128;
+    b.dk = h == 0 ? 128 : static_cast<int>(dk) - 128;  // the second half may be narrower (padded)
     b.q = static_cast<const uint16_t*>(a.q) + 128 * h;
     b.k = static_cast<const uint16_t*>(a.k) + 128 * h;
     for (int t = 0; t < 2; ++t) b.rp[t] = a.rp[t] ? a.rp[t] : dk;
@@ -208,7 +210,10 @@ static int run_f_split_d(const FArgs& a, cudaStream_t st) {
 }
 
 static int run_f(const FArgs& a, cudaStream_t st) {
-  if (tc_eligible(a.dtype, a.dk, a.dv)) return a.dk == 256 ? run_f_split_d(a, st) : launch_tc(a, st);
+  // a transposed carried state is read with compile-time row strides (the kernel's DK or
+  // 256); a padded head dim with one runs that pass on the SIMT kernel
+  const bool padded_T = a.kv_in != nullptr && a.kv_in_T && a.dk != 64 && a.dk != 128 && a.dk != 256;
+  if (tc_eligible(a.dtype, a.dk, a.dv) && !padded_T) return a.dk > 128 ? run_f_split_d(a, st) : launch_tc(a, st);
   return launch_simt(a, st);
 }
 
@@ -222,8 +227,8 @@ static int check_common(int B, int H, int N, int d, int dv, int dtype, const flo
   if (!tc_eligible(dtype, d, dv) && (d > 256 || dv > 256)) {
     char buf[160];
     std::snprintf(buf, sizeof(buf),
-                  "unsupported shape d=%d dv=%d for dtype %s (bf16 tensor-core path: d in "
-                  "{64,128,256}, dv %% 64 == 0; otherwise d, dv <= 256)",
+                  "unsupported shape d=%d dv=%d for dtype %s (bf16 tensor-core path: d, dv "
+                  "multiples of 8 up to 256; otherwise d, dv <= 256)",
                   d, dv, dtype == LA2_BF16 ? "bf16" : "fp32");
     return set_error(LA2_ERR_UNSUPPORTED, buf);
   }
@@ -293,7 +298,7 @@ int la2_forward_strided(const void* q, const void* k, const void* v, const float
   if (!q || !k || !v || !o) return set_error(LA2_ERR_VALUE, "null tensor pointer");
   if (!tc_eligible(dtype, d, dv))
     return set_error(LA2_ERR_UNSUPPORTED,
-                     "strided inputs need the tensor-core path (bf16, d in {64,128,256}, dv % 64 == 0)");
+                     "strided inputs need the tensor-core path (bf16, d and dv multiples of 8 up to 256)");
   const long long need[3] = {1LL * N * d, 1LL * N * d, 1LL * N * dv};
   const long long ld[3] = {ldq, ldk, ldv};
   for (int t = 0; t < 3; ++t)
@@ -342,7 +347,7 @@ int la2_backward_strided(const void* q, const void* k, const void* v, const void
   g_err[0] = 0;
   if (!tc_eligible(dtype, d, dvd))
     return set_error(LA2_ERR_UNSUPPORTED,
-                     "strided inputs need the tensor-core path (bf16, d in {64,128,256}, dv % 64 == 0)");
+                     "strided inputs need the tensor-core path (bf16, d and dv multiples of 8 up to 256)");
   const long long ld[4] = {ldq, ldk, ldv, lddo};
   const long long need[4] = {1LL * N * d, 1LL * N * d, 1LL * N * dvd, 1LL * N * dvd};
   for (int t = 0; t < 4; ++t)

@@ -69,6 +69,7 @@ struct FParams {
   int kv_in_rs, kv_out_rs;
   int accum;  // output epilogue: TMA reduce-add into o
   int store_states;  // forward (d = 64): write the per-block bf16 states through tm_v1
+  int dkr;           // real head dim of the pass (<= the kernel's DK; rows beyond it are padding)
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);

@@ -891,15 +891,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int j = 0; j < KVC; ++j) kv[j] = 0.f;
       if (pos == 0) {
-        if (p.kv_in != nullptr && has_kv) {
+        // (rows >= the real head dim / columns >= the real value width are padding: 0)
+        if (p.kv_in != nullptr && has_kv && kvrow < p.dkr) {
           const size_t sbase = static_cast<size_t>(bh) * p.kv_in_bhs;
           const int c0 = slice * DVS + kc0;
           if (!kv_in_T) {
             const float* src = p.kv_in + sbase + static_cast<size_t>(kvrow) * p.kv_in_rs + c0;
 #pragma unroll
             for (int j = 0; j < KVC; j += 4) {
-              float4 w = *reinterpret_cast<const float4*>(src + j);
-              kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
+              if (c0 + j < p.dv_total) {
+                float4 w = *reinterpret_cast<const float4*>(src + j);
+                kv[j] = w.x; kv[j + 1] = w.y; kv[j + 2] = w.z; kv[j + 3] = w.w;
+              }
             }
           } else {
             // state stored transposed: element (r, c) at c * rs + r
@@ -936,12 +939,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // state for the next work range (which continues this unit).
     auto store_state = [&](int bh, int slice, int pos) {
       if (pos == nblk - 1) {
-        if (kv_out != nullptr && has_kv) {
+        if (kv_out != nullptr && has_kv && kvrow < p.dkr) {
           float* dst = kv_out + static_cast<size_t>(bh) * p.kv_out_bhs +
                        static_cast<size_t>(kvrow) * p.kv_out_rs + slice * DVS + kc0;
 #pragma unroll
           for (int j = 0; j < KVC; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
+            if (slice * DVS + kc0 + j < p.dv_total)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]);
         }
       } else {
         const int slot = cid * CS + static_cast<int>(crank);
@@ -1269,7 +1273,11 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   const void* ptrs[8] = {a.q, a.k, a.v, a.o, a1 ? a1->q : a.q, a1 ? a1->k : a.k,
                          a1 ? a1->v : a.v, a1 ? a1->o : a.o};
   CUtensorMap* maps[8] = {&mq, &mk, &mv, &mo, &mq1, &mk1, &mv1, &mo1};
-  const int cols[8] = {DK, DK, a.dv, a.dv, DK, DK, a.dv, a.dv};
+  // real operand widths: a q / k narrower than the kernel's DK (or a v / o whose last 64-wide
+  // slice is partial) reads as zero beyond its width (TMA out-of-bounds fill) and stores
+  // clip there, so any width that is a multiple of 8 runs padded on the tensor cores
+  const int cols[8] = {a.dk, a.dk, a.dv, a.dv, a1 ? a1->dk : a.dk, a1 ? a1->dk : a.dk, a1 ? a1->dv : a.dv,
+                       a1 ? a1->dv : a.dv};
   for (int t = 0; t < 8; ++t) {
     if (SO && t != 1 && t != 2) continue;
     if (CM != 3 && (t == 5 || t == 6)) continue;
@@ -1304,11 +1312,11 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
-  p.kv_in_bhs = a.kv_in_bhs ? a.kv_in_bhs : static_cast<long long>(DK) * a.dv;
-  p.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : (a.kv_in_T ? DK : a.dv);
+  p.kv_in_bhs = a.kv_in_bhs ? a.kv_in_bhs : static_cast<long long>(a.dk) * a.dv;
+  p.kv_in_rs = a.kv_in_rs ? a.kv_in_rs : (a.kv_in_T ? a.dk : a.dv);
   if (a.kv_in != nullptr && a.kv_in_T && p.kv_in_rs != DK && p.kv_in_rs != 256)
     return set_error(LA2_ERR_UNSUPPORTED, "transposed state row stride must be the head dim or 256");
-  p.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : static_cast<long long>(DK) * a.dv;
+  p.kv_out_bhs = a.kv_out_bhs ? a.kv_out_bhs : static_cast<long long>(a.dk) * a.dv;
   p.kv_out_rs = a.kv_out_rs ? a.kv_out_rs : a.dv;
   p.accum = a.accum_o;
   p.store_states = store_states ? 1 : 0;
@@ -1316,7 +1324,8 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   p.hint = l2_hints();
   // persistent schedule: units = independent recurrences (a cluster's pair counts once)
   constexpr int CS = (CM == 3) ? 4 : ((CM == 4) ? 3 : (CM ? 2 : 1));
-  p.nsl = a.dv / DVS;
+  p.nsl = (a.dv + DVS - 1) / DVS;
+  p.dkr = a.dk;
   p.units = (CM == 2 || CM == 4) ? BH : ((CM == 1 || CM == 3) ? BH * p.nsl / 2 : BH * p.nsl);
   p.P = p.units;
   p.ws = nullptr;
@@ -1399,9 +1408,9 @@ int launch_tc(const FArgs& a, cudaStream_t st) {
   if (get_encode() != 0) return set_error(LA2_ERR_CUDA, "cannot resolve cuTensorMapEncodeTiled");
   const bool so = (a.o == nullptr);
   // value-slice pairs share their Q/K tiles through a 2-CTA cluster
-  const bool pair = clusters_enabled() && (a.dv / DVS) % 2 == 0;
+  const bool pair = clusters_enabled() && ((a.dv + DVS - 1) / DVS) % 2 == 0;
 #define LA2_TC_DISPATCH(DKV)                                                                   \
-  if (a.dk == DKV) {                                                                           \
+  if ((a.dk <= 64 ? 64 : 128) == DKV) {                                                      \
     if (so && pair) return a.reverse ? launch_tc_t<DKV, true, true, 1>(a, st)                  \
                                      : launch_tc_t<DKV, false, true, 1>(a, st);                \
     if (so) return a.reverse ? launch_tc_t<DKV, true, true, 0>(a, st)                          \
@@ -1414,7 +1423,7 @@ int launch_tc(const FArgs& a, cudaStream_t st) {
   LA2_TC_DISPATCH(64)
   LA2_TC_DISPATCH(128)
 #undef LA2_TC_DISPATCH
-  return set_error(LA2_ERR_UNSUPPORTED, "tensor-core path supports head dim 64 or 128");
+  return set_error(LA2_ERR_UNSUPPORTED, "tensor-core path supports head dims up to 128 per pass");
 }
 
 // The two reverse scans of the backward pass (dV = F_rev(K, Q, dO), dK = F_rev(V, dO, Q))

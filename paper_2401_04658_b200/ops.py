@@ -171,7 +171,10 @@ def _state(t: Optional[torch.Tensor], B, H, d, dv, device, name, dtype=torch.flo
 
 # ------------------------------------------------------ intra-GPU sequence split
 NUM_SMS = 148
-TC_DIMS = (64, 128, 256)  # bf16 head dims on the tensor-core kernel (256: split-d, include/la2.h)
+def tc_shape(d: int, dv: int) -> bool:
+    """bf16 widths on the tensor-core kernels (include/la2.h): d and dv multiples of 8 up to
+    256 (d <= 128 padded to 64 / 128, d > 128 as split-d, dv in 64-wide slices)."""
+    return 8 <= d <= 256 and d % 8 == 0 and 8 <= dv <= 256 and dv % 8 == 0
 MAX_CHUNKS = 64  # la2_state_scan combines at most 64 chunk states per call
 
 
@@ -193,7 +196,7 @@ def split_factor(B: int, H: int, N: int, d: int, dv: int, dtype) -> int:
         return 1  # the fp64 correctness path runs unsplit
     units = B * H * ((dv + 63) // 64)
     g = 1
-    if dtype == torch.bfloat16 and d in TC_DIMS and dv % 64 == 0 and dv <= 256:
+    if dtype == torch.bfloat16 and tc_shape(d, dv):
         if units >= 100:
             return 1
         while (units * g < NUM_SMS and 2 * g <= MAX_CHUNKS and N % (2 * g * 128) == 0
@@ -281,7 +284,7 @@ def la2_forward(q, k, v, decay: DecayLike, kv_in: Optional[torch.Tensor] = None,
     kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
     kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
     lds = None
-    if q.dtype == torch.bfloat16 and d in TC_DIMS and dv % 64 == 0 and not (
+    if q.dtype == torch.bfloat16 and tc_shape(d, dv) and not (
             q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
         lds = [_head_stride(t) for t in (q, k, v)]
         if any(x is None for x in lds):
@@ -396,7 +399,7 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     dkv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_dkv else None
     ts = (q, k, v, d_out)
     lds = None
-    if q.dtype == torch.bfloat16 and d in TC_DIMS and dv % 64 == 0 and not all(t.is_contiguous() for t in ts):
+    if q.dtype == torch.bfloat16 and tc_shape(d, dv) and not all(t.is_contiguous() for t in ts):
         lds = [_head_stride(t) for t in ts]
         if any(x is None for x in lds):
             lds = None

@@ -810,7 +810,7 @@ def test_forward_strided_abi_errors():
     assert call(N * d - 8) == _lib.LA2_ERR_VALUE
     assert call(N * d + 4) == _lib.LA2_ERR_VALUE
     assert call(N * d, dt=1) == _lib.LA2_ERR_UNSUPPORTED
-    assert call(N * 32, dd=32) == _lib.LA2_ERR_UNSUPPORTED
+    assert call(N * 12, dd=12) == _lib.LA2_ERR_UNSUPPORTED  # not a multiple of 8: no TMA path
     torch.cuda.synchronize()
 
 
@@ -1066,3 +1066,44 @@ def test_fp64_invalid_decay_raises():
         la2.lightning_attn2(*gpu(q, k, v), [0.5, 1.5])
     with pytest.raises(ValueError):
         la2.lightning_attn2(*gpu(q, k, v), torch.tensor([0.5, 0.0], dtype=torch.float64, device=DEV))
+
+
+# ---------------------------------------------- padded widths on the tensor cores
+@pytest.mark.parametrize("d,dv", [(32, 32), (96, 96), (64, 40), (16, 200), (160, 96), (192, 64), (8, 8)])
+def test_padded_widths_on_tensor_cores(d, dv):
+    """bf16 widths that are multiples of 8 but not of 64 run on the tcgen05 kernels, the
+    operands zero-padded by the TMA unit (out-of-bounds fill) and the stores clipped;
+    d > 128 as split-d with a narrower second half. With carried state in and out."""
+    B, H, N = 1, 3, 700
+    decay = [0.5, 0.99, 1.0]
+    q, k, v, do = inputs(B, H, N, d, dv, torch.bfloat16, seed=d + dv)
+    kv0 = rand((B, H, d, dv), 7, torch.float32)
+    la2.ops.launch_log(64)
+    o, kv = la2.la2_forward(*gpu(q, k, v), decay, kv_in=kv0.to(DEV), output_final_state=True)
+    dq, dk, dv_, _ = la2.la2_backward(*gpu(q, k, v, do), decay)
+    log = la2.ops.read_launch_log()
+    la2.ops.launch_log(0)
+    assert log and all(r["kernel"].startswith("la2_tc_kernel") for r in log), log
+    Q, K, V, DO = (to64(t) for t in (q, k, v, do))
+    ro, rkv = port.bhnd_forward(Q, K, V, decay, block=64, kv_in=kv0.double().numpy())
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay, block=64)
+    errs = {"o": rel(o, ro), "kv": rel(kv, rkv), "dq": rel(dq, rq), "dk": rel(dk, rk), "dv": rel(dv_, rv)}
+    print(d, dv, errs)
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_padded_width_autograd_long_split():
+    """A padded width (d = dv = 96) on a long few-head sequence: the intra-GPU split
+    (state-only pass, scan, carried pass) on the padded tensor-core kernels."""
+    B, H, N, d = 1, 2, 65536, 96
+    decay = [0.9999, 1.0]
+    q, k, v, do = inputs(B, H, N, d, d, torch.bfloat16, seed=3)
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    o = la2.lightning_attn2(qg, kg, vg, decay)
+    o.backward(do.to(DEV))
+    Q, K, V, DO = (to64(t) for t in (q, k, v, do))
+    ro, _ = port.bhnd_forward(Q, K, V, decay, block=256)
+    rq, rk, rv = port.bhnd_backward(Q, K, V, DO, decay, block=256)
+    errs = {"o": rel(o, ro), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
+    print(errs)
+    assert max(errs.values()) <= BF16_TOL, errs
