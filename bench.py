@@ -14,9 +14,11 @@ the same run and reported under "sweep". Inputs are synthetic
 Multi-GPU (torchrun): each rank runs its own B=8 batch (batch x head sharding,
 no collective on the data path, "scaling": "weak"); time = max over ranks.
 
---impl reference: the reference's CPU algorithm (the oracle port of
-pkg/src/tila/kernel.py, numpy/OpenBLAS) on all host cores of rank 0, over a
-bounded sample of the same workload, extrapolated to the same metric.
+--impl reference: the reference's own CPU implementation (tila.tiled_forward /
+tiled_backward from oracle/_ref/tila, the unmodified package staged by build(); the
+oracle port of pkg/src/tila/kernel.py if it is absent), numpy/OpenBLAS on all host
+cores of rank 0, over a bounded sample of the same workload, extrapolated to the same
+metric.
 """
 
 from __future__ import annotations
@@ -127,17 +129,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU side
+REF_PKG = ROOT / "oracle" / "_ref"  # the reference package itself, staged by build()
+
+
+def _reference_impl():
+    """The reference's own tiled_forward / tiled_backward (oracle/_ref/tila, staged by
+    build() from /root/reference) when present, else the oracle port's restatement."""
+    if (REF_PKG / "tila" / "kernel.py").exists():
+        if str(REF_PKG) not in sys.path:
+            sys.path.insert(0, str(REF_PKG))
+        import tila
+
+        return tila, "reference"
+    from oracle import tila_port as port
+
+    return port, "port"
+
+
 def _cpu_head_task(args):
     n, d, seed, lam = args
     import numpy as np
 
-    from oracle import tila_port as port
-
+    impl, _ = _reference_impl()
     rng = np.random.default_rng(seed)
     q, k, v, do = (rng.uniform(-1, 1, (n, d)).astype(np.float32) for _ in range(4))
     t0 = time.perf_counter()
-    port.tiled_forward(q, k, v, lam, 64)
-    port.tiled_backward(q, k, v, do, lam, 64)
+    impl.tiled_forward(q, k, v, lam, 64)
+    impl.tiled_backward(q, k, v, do, lam, 64)
     return time.perf_counter() - t0
 
 
@@ -164,8 +182,10 @@ def cpu_reference(n: int, d: int, heads_total: int, tokens_per_step: int, sample
             walls.append(time.perf_counter() - t0)
     wall = statistics.median(walls)
     t_full = wall * heads_total / sample_heads
-    return {"value": tokens_per_step / t_full, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{sample_heads} heads x N={n} d={d} fp32 fwd+bwd (tila block loop, block=64), "
+    kind = _reference_impl()[1]
+    return {"value": tokens_per_step / t_full, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{sample_heads} heads x N={n} d={d} fp32 fwd+bwd "
+                      f"({'the reference tila.tiled_forward/tiled_backward' if kind == 'reference' else 'oracle port of the tila block loop'}, block=64), "
                       f"{cores} processes, median of {reps}; extrapolated x{heads_total / sample_heads:.1f} "
                       f"to B*H={heads_total}",
             "sample_wall_s": wall}
