@@ -90,12 +90,20 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #ifndef LA2_SO_NS
 #define LA2_SO_NS 4
 #endif
+// d = 128 full passes: Q/K and V in separate rings (2 and 3 deep, one V~ buffer) instead of
+// 2 stages of Q|K|V -- V is read last (PV needs the row warps' P), so a third V slot keeps
+// the next block's loads in flight while Q/K recycle as soon as S, the fold and Oe read them
+#ifndef LA2_SPLIT_RING
+#define LA2_SPLIT_RING 0
+#endif
 
 template <int DK, bool SO, bool TRI = false>
 struct TcLayout {
   // Q/K/V stages; state-only passes stage only K and V (32 / 48 KB), so they get a deeper ring
   static constexpr int NS = SO ? LA2_SO_NS : ((DK == 64) ? 3 : 2);
-  static constexpr int KTS = 2;                   // V~ buffers (scaled values)
+  static constexpr bool RING2 = (NS == 2) && !SO && (LA2_SPLIT_RING != 0);  // split Q/K | V rings
+  static constexpr int NSV = RING2 ? 3 : NS;      // V ring depth
+  static constexpr int KTS = RING2 ? 1 : 2;       // V~ buffers (scaled values)
   // O staging buffers (the backward triple spends the second one on its state tiles)
   static constexpr int OS = (DK == 64 && !SO && !TRI) ? 2 : 1;
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
@@ -107,7 +115,7 @@ struct TcLayout {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
-  static constexpr int OFF_S = OFF_V + NS * V_BYTES;
+  static constexpr int OFF_S = OFF_V + NSV * V_BYTES;
   static constexpr int OFF_KT = OFF_S + NS * S_BYTES;
   static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
   // second bf16 state-operand buffer of the backward pair / triple's shared recurrence
@@ -120,6 +128,7 @@ struct TcLayout {
   static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
   static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
+  static constexpr uint32_t QK_TX = Q_BYTES + K_BYTES;  // RING2: the Q/K ring's share
   // TMEM columns. OIS ("O in S", d = 128): S[b] @128b holds the scores, then P (packed
   // bf16, cols +0..63) and O_i = P_i V_i (fp32, cols +64..127), so O is double-buffered
   // with S and PV_i does not wait for the epilogue of block i-1 | Oe[2] @256,320 |
@@ -136,7 +145,9 @@ struct TcLayout {
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
   static constexpr uint32_t T_O = 256, T_OE = OIS ? 256 : 320, T_KV = SO ? 0 : 384;
   // barrier slots
-  static constexpr int B_FULL = 0, B_EMPTY = NS, B_SFULL = 2 * NS, B_SFREE = B_SFULL + 2,
+  // (RING2: B_FULL / B_EMPTY guard the Q/K ring, B_FULLV / B_EMPTYV the V ring)
+  static constexpr int B_FULL = 0, B_EMPTY = NS, B_FULLV = 2 * NS, B_EMPTYV = B_FULLV + NSV,
+                       B_SFULL = B_EMPTYV + NSV, B_SFREE = B_SFULL + 2,
                        B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEFULL = B_OFULL + 2,
                        B_OEMPTY = B_OEFULL + 2, B_KTREADY = B_OEMPTY + 2, B_KTFREE = B_KTREADY + KTS,
                        B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 2,
@@ -228,6 +239,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
+    if (L::RING2) {
+      for (int s = 0; s < L::NSV; ++s) {
+        mbar_init(&bars[L::B_FULLV + s], 1);
+        mbar_init(&bars[L::B_EMPTYV + s], 2);  // X after PV, Y after the fold (V~ copy done); local
+      }
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[L::B_FULL + s], 1);
       // X after PV, Y after Oe (x2 in a cluster: the stage is shared)
@@ -283,7 +300,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // With a 2-stage ring (d = 128: 80 KB stages) a stage is refilled only one block
       // ahead, which exposes HBM latency; pull the next PF blocks into L2 so the ring's
       // TMA loads hit L2.
-      const int PF = (NS == 2) ? p.pf : 0;
+      const int PF = (NS == 2 && !L::RING2) ? p.pf : 0;
       const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
       auto tma_prefetch_l2_3d = [&](const CUtensorMap* m, int c0, int c1, int c2) {
         if (p.hint & 2) la2::tma_prefetch_l2_3d_hint(m, c0, c1, c2, pol_last);
@@ -351,19 +368,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      ((w.pos == nblk - 1 || g == sch.npre - 1) ? REC_SEG_END : 0);
           recs[g & 7] = rc;
         }
-        mbar_arrive_expect_tx(&bars[L::B_FULL + s], dqr ? L::STAGE_TX + L::S_BYTES : L::STAGE_TX);
+        mbar_arrive_expect_tx(&bars[L::B_FULL + s],
+                              L::RING2 ? L::QK_TX : (dqr ? L::STAGE_TX + L::S_BYTES : L::STAGE_TX));
         const int row = blk * BT;
         uint64_t* fb = &bars[L::B_FULL + s];
         uint8_t* dq = smem + L::OFF_Q + s * L::Q_BYTES;
         uint8_t* dk = smem + L::OFF_K + s * L::K_BYTES;   // stage region "K" (tile of tm_k)
         uint8_t* dv = smem + L::OFF_V + s * L::V_BYTES;   // stage region "V" (tile of tm_v)
+        uint64_t* fbv = fb;                                // the V tile's barrier
+        if (L::RING2) {
+          // V ring: slot g % NSV, refilled once X's PV and Y's fold of block g - NSV are done
+          const int sv = g % L::NSV;
+          if (g >= L::NSV) mbar_wait(&bars[L::B_EMPTYV + sv], ((g / L::NSV) - 1) & 1);
+          fbv = &bars[L::B_FULLV + sv];
+          mbar_arrive_expect_tx(fbv, L::V_BYTES);
+          dv = smem + L::OFF_V + sv * L::V_BYTES;
+        }
         if (CM == 0) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
             if (!SO) tma_load_3d(dq + c * REGION, mq, fb, c * 64, row, bh);
             tma_load_3d(dk + c * REGION, &tm_k, fb, c * 64, row, bh);
           }
-          tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
+          tma_load_3d(dv, &tm_v, fbv, slice * DVS, row, bh);
         } else if (CM == 1 || CM == 3) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
@@ -373,7 +400,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_3d_mc(dk + c * REGION, mk, fb, c * 64, row, bh, mcmask);
             }
           }
-          tma_load_3d(dv, mv, fb, slice * DVS, row, bh);
+          tma_load_3d(dv, mv, fbv, slice * DVS, row, bh);
         } else if (CM == 2) {
           tma_load_3d(dq, mq, fb, 0, row, bh);  // own q: K (rank 0) or V (rank 1)
           if (crank == 0) tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K
@@ -500,7 +527,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      (nS < 2 || mbar_test(&bars[L::B_SFREE + (nS & 1)], ((nS >> 1) - 1) & 1));
             if (nP < nS)
               p_ok = mbar_test(&bars[L::B_PREADY + (nP & 1)], (nP >> 1) & 1) &&
-                     (L::OIS || nP == 0 || mbar_test(&bars[L::B_OEMPTY + ((nP - 1) & 1)], ((nP - 1) >> 1) & 1));
+                     (L::OIS || nP == 0 || mbar_test(&bars[L::B_OEMPTY + ((nP - 1) & 1)], ((nP - 1) >> 1) & 1)) &&
+                     (!L::RING2 || mbar_test(&bars[L::B_FULLV + nP % L::NSV], (nP / L::NSV) & 1));
           }
           s_ok = __shfl_sync(0xffffffffu, s_ok, 0);
           p_ok = __shfl_sync(0xffffffffu, p_ok, 0);
@@ -520,12 +548,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
               }
               umma_commit(&bars[L::B_SFULL + b]);
+              if (L::RING2) commit_empty(s);  // X's last read of the Q/K slot
             }
             ++nS;
           }
           if (p_ok) {
             const int s = nP % NS, b = nP & 1;
-            const uint64_t v = adv(dV0, s * L::V_BYTES);
+            const uint64_t v = adv(dV0, (L::RING2 ? nP % L::NSV : s) * L::V_BYTES);
             TR(1, nP, 3);
             if (leader) {
 #pragma unroll
@@ -536,7 +565,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               }
               if (!L::OIS) umma_commit(&bars[L::B_SFREE + b]);
               umma_commit(&bars[L::B_OFULL + b]);
-              commit_empty(s);
+              if (L::RING2) umma_commit(&bars[L::B_EMPTYV + nP % L::NSV]);  // the V slot
+              else commit_empty(s);
             }
             ++nP;
           }
@@ -560,6 +590,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma_commit(&bars[L::B_DKVFULL + db]);
           umma_commit(&bars[L::B_KTFREE + kt]);
           if (SO) commit_empty(s);
+          // the V~ copy of block i (done before KTREADY) was the V slot's other reader
+          if (L::RING2) umma_commit(&bars[L::B_EMPTYV + i % L::NSV]);
         }
         __syncwarp();
       };
@@ -1124,8 +1156,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // V~_j = c . V_j (c_t = lam^(r-1-t), rev: lam^(t+1)), the fold operand of dKV_j. Off
     // the state warps, whose state update of block j-1 then overlaps this copy.
     for (int j = 0; j < T; ++j) {
-      const int s = j % NS, kt = j % KTS;
-      mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+      // (RING2: the V slot of block j has its own barrier; it is published after the record)
+      const int s = L::RING2 ? j % L::NSV : j % NS, kt = j % KTS;
+      if (L::RING2) mbar_wait(&bars[L::B_FULLV + s], (j / L::NSV) & 1);
+      else mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
       const BlkRec rc = recs[j & 7];
       const int r = min(BT, N - rc.blk * BT);
       if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
