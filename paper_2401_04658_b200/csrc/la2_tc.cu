@@ -93,6 +93,11 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 // d = 128 full passes: Q/K and V in separate rings (2 and 3 deep, one V~ buffer) instead of
 // 2 stages of Q|K|V -- V is read last (PV needs the row warps' P), so a third V slot keeps
 // the next block's loads in flight while Q/K recycle as soon as S, the fold and Oe read them
+// d = 128 full passes: double-buffer the bf16 state operand (one V~ buffer pays for it),
+// so writing KV_i waits for Oe_{i-1} instead of Oe_i
+#ifndef LA2_KV2_128
+#define LA2_KV2_128 0
+#endif
 #ifndef LA2_SPLIT_RING
 #define LA2_SPLIT_RING 0
 #endif
@@ -103,7 +108,8 @@ struct TcLayout {
   static constexpr int NS = SO ? LA2_SO_NS : ((DK == 64) ? 3 : 2);
   static constexpr bool RING2 = (NS == 2) && !SO && (LA2_SPLIT_RING != 0);  // split Q/K | V rings
   static constexpr int NSV = RING2 ? 3 : NS;      // V ring depth
-  static constexpr int KTS = RING2 ? 1 : 2;       // V~ buffers (scaled values)
+  static constexpr bool DBL128 = (DK == 128) && !SO && !RING2 && (LA2_KV2_128 != 0);
+  static constexpr int KTS = (RING2 || DBL128) ? 1 : 2;  // V~ buffers (scaled values)
   // O staging buffers (the backward triple spends the second one on its state tiles)
   static constexpr int OS = (DK == 64 && !SO && !TRI) ? 2 : 1;
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
@@ -120,7 +126,7 @@ struct TcLayout {
   static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
   // second bf16 state-operand buffer of the backward pair / triple's shared recurrence
   // (LA2_SPLIT_STATE): the triple's ranks 0-1 use their (otherwise idle) state-tile ring
-  static constexpr bool KV2 = (DK == 64) && !SO && !TRI;
+  static constexpr bool KV2 = ((DK == 64) && !SO && !TRI) || DBL128;
   static constexpr int OFF_O = OFF_KV + (KV2 ? 2 : 1) * KV_BYTES;
   static constexpr int OFF_KV2 = TRI ? OFF_S : OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
@@ -621,7 +627,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                adv(dk, (kk >> 1) * 4096 + (kk & 1) * 32), ID_OS, kk > 0);
               }
             } else {
-              const uint64_t kvd = dKV0;
+              const uint64_t kvd = (L::DBL128 && (i & 1)) ? sdesc_sw128(smem_u32(smem + L::OFF_KV2), DK * 128, 1024)
+                                                           : dKV0;
 #pragma unroll
               for (int kk = 0; kk < DK / 16; ++kk)
                 umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
@@ -662,6 +669,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (!SO) {
           // SPLIT: KV_{i-1} sits in operand buffer i & 1, half of it written by the peer
           if (SPLIT) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
+          else if (L::DBL128) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
           else mbar_wait(&bars[L::B_KVREADY], i & 1);
           if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
           if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
@@ -1050,13 +1058,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           else mbar_arrive(&bars[L::B_KVREADY + b]);
         }
       } else {
+        uint8_t* dst = (L::DBL128 && b) ? smem + L::OFF_KV2 : sKVb;
         if (has_kv) {
 #pragma unroll
-          for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(sKVb, kvrow, q, kv + 16 * q);
+          for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(dst, kvrow, q, kv + 16 * q);
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
+        if (lane == 0) mbar_arrive(&bars[L::B_KVREADY + (L::DBL128 ? b : 0)]);
       }
     };
     if (!SO) {
@@ -1135,7 +1144,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (SPLIT) {
             if (i >= 1) mbar_wait(&bars[L::B_KVFREE + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           }
-          else if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
+          else if (L::DBL128) {  // buffer (i + 1) & 1 was last read by Oe_{i-1}
+            if (i >= 1) mbar_wait(&bars[L::B_OEFULL + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
+          } else if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (GW) named_bar_sync(5, 128);
           if (st_states) {  // the previous block's state store has read the operand buffer
             if (warp == W0 && lane == 0) tma_store_wait_read<0>();
