@@ -128,3 +128,35 @@ def test_dev_library_is_separate(lib):
     for name in dev_syms:
         assert hasattr(dev, name), name
         assert not hasattr(lib, name), name
+
+
+def test_f64_entry_points_validate_without_device(lib):
+    """The double-precision entry points (la2_*_f64) reject bad shapes / nulls before any
+    device work, and la2_check_decay_f64 validates host decay like the reference."""
+    from paper_2401_04658_b200 import _lib
+
+    dummy = ctypes.c_void_p(16)
+    assert lib.la2_forward_f64(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 0, 4, 4, 0,
+                               None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_forward_f64(dummy, dummy, dummy, None, dummy, None, None, 1, 1, 8, 4, 4, 0,
+                               None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_forward_f64(dummy, dummy, dummy, dummy, dummy, None, None, 1, 1, 8, 300, 4, 0,
+                               None) == _lib.LA2_ERR_UNSUPPORTED
+    assert lib.la2_backward_f64(dummy, dummy, dummy, dummy, dummy, None, dummy, dummy, None, None, None,
+                                1, 1, 8, 4, 4, 0, None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_decode_step_f64(dummy, dummy, dummy, dummy, None, dummy, 1, 1, 4, 4,
+                                   None) == _lib.LA2_ERR_VALUE
+    good = (ctypes.c_double * 3)(0.5, 1.0, 1e-300)
+    assert lib.la2_check_decay_f64(good, 3, None) == 0
+    for vals in ((0.5, 1.0000000001), (0.5, 0.0), (0.5, float("nan"))):
+        arr = (ctypes.c_double * 2)(*vals)
+        assert lib.la2_check_decay_f64(arr, 2, None) == _lib.LA2_ERR_VALUE
+        assert b"head 1" in lib.la2_last_error()
+
+
+def test_tensor_core_envelope_documented():
+    """The header's kernel-selection rule names the widened bf16 envelope (multiples of 8
+    up to 256) and the fp64 entry points."""
+    text = HEADER.read_text()
+    assert "multiples of 8 up to 256" in text
+    assert "la2_forward_f64" in text and "la2_backward_f64" in text
