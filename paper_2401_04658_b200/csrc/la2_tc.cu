@@ -1237,6 +1237,20 @@ static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, i
   }
   return rc;
 }
+// L2 sector promotion of the TMA loads (development knob LA2_L2PROMO: 0 none, 1 64 B,
+// 2 128 B, 3 256 B = default)
+static CUtensorMapL2promotion l2_promotion() {
+  static const int v = [] {
+    const char* e = std::getenv("LA2_L2PROMO");
+    return e ? std::atoi(e) : 3;
+  }();
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows,
                    long long head_stride, long long row_pitch) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
@@ -1249,7 +1263,7 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r) - 1000;
 }
