@@ -44,25 +44,37 @@ Workspace get_workspace(cudaStream_t st) {
   for (const Entry& e : cache)
     if (e.dev == dev && e.st == st) return e.w;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
     cudaGetLastError();
     return Workspace{nullptr, nullptr, 0};
   }
+  const bool capturing = (cap != cudaStreamCaptureStatusNone);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int slots = sms;  // at most one CTA per SM
   const size_t state_bytes = workspace_state_bytes(slots);
   void* buf = nullptr;
-  if (cudaMalloc(&buf, state_bytes + slots * sizeof(int)) != cudaSuccess) {
-    cudaGetLastError();
-    return Workspace{nullptr, nullptr, 0};
-  }
-  int* flags = reinterpret_cast<int*>(static_cast<char*>(buf) + state_bytes);
+  // First use of a stream inside CUDA-graph capture: allocate and zero the workspace
+  // outside the capture (relaxed capture mode for this thread, a private stream for the
+  // zeroing), so captured launches keep the persistent schedule -- without it they run
+  // one CTA per recurrence, up to 1.7x slower (tools/graphed_step.py).
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  if (capturing) cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaStream_t zs = st;
+  bool ok = cudaMalloc(&buf, state_bytes + slots * sizeof(int)) == cudaSuccess;
+  int* flags = ok ? reinterpret_cast<int*>(static_cast<char*>(buf) + state_bytes) : nullptr;
+  if (ok && capturing) ok = cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking) == cudaSuccess;
   // zeroed on the stream that will use it (a legacy-stream memset would not be ordered
-  // before kernels on non-blocking streams)
-  if (cudaMemsetAsync(flags, 0, slots * sizeof(int), st) != cudaSuccess) {
+  // before kernels on non-blocking streams), or on the private stream, waited for
+  if (ok) ok = cudaMemsetAsync(flags, 0, slots * sizeof(int), zs) == cudaSuccess;
+  if (ok && capturing) {
+    ok = cudaStreamSynchronize(zs) == cudaSuccess;
+    cudaStreamDestroy(zs);
+  }
+  if (capturing) cudaThreadExchangeStreamCaptureMode(&mode);
+  if (!ok) {
     cudaGetLastError();
-    cudaFree(buf);
+    if (buf) cudaFree(buf);
     return Workspace{nullptr, nullptr, 0};
   }
   Workspace w{static_cast<float*>(buf), flags, slots};
