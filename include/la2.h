@@ -9,8 +9,8 @@
  * library never allocates, frees or retains caller memory. Its only own device
  * memory is one fixed workspace per (device, stream) -- the stream-K state
  * hand-off slots, la2_workspace_bytes() bytes (~4.7 MB on B200), allocated on the
- * first launch on that stream outside graph capture and kept for the process
- * lifetime; it does not grow with B, H or N. A CUDA graph captured on a stream bakes
+ * first launch on that stream (outside the capture when that launch is being captured
+ * into a CUDA graph) and kept for the process lifetime; it does not grow with B, H or N. A CUDA graph captured on a stream bakes
  * in that stream's workspace: replays of graphs captured on the same stream must not
  * run concurrently with each other (capture concurrent graphs on distinct streams).
  *
