@@ -84,7 +84,7 @@ int launch_tc_quad(const FArgs& adv, const FArgs& adk, cudaStream_t st);
 // head_stride = elements between (b, h) rows (0: N * cols).
 int tma_encoder_ready();
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows, long long head_stride = 0,
-                   long long row_pitch = 0);
+                   long long row_pitch = 0, int box_cols = 64);
 int launch_simt(const FArgs& a, cudaStream_t st);
 // fp64 F pass (la2_f64.cu): one launch of the block recurrence (reverse = F_rev) and
 // the fp64 decode step

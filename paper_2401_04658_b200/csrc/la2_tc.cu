@@ -98,6 +98,12 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #ifndef LA2_KV2_128
 #define LA2_KV2_128 0
 #endif
+// Output epilogue: each row warp stages and TMA-stores its own [32 rows][32 cols] tile
+// (SW64, box 32 x 32) instead of the quarter's two warps meeting at two named barriers
+// around one [32][64] store
+#ifndef LA2_WARP_STORE
+#define LA2_WARP_STORE 1
+#endif
 #ifndef LA2_SPLIT_RING
 #define LA2_SPLIT_RING 0
 #endif
@@ -853,7 +859,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const bool storer = (half == 0 && lane == 0);
           if (warp == LA2_TRW) TR(2, i, 3);
           const int ob = i & 1;
-          if (GW) {
+          if (LA2_WARP_STORE) {
+            if (lane == 0) tma_store_wait_read<OS - 1>();  // this warp's previous store read sW
+            __syncwarp();
+            mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
+            mbar_wait(&bars[L::B_OEFULL + ob], (i >> 1) & 1);
+          } else if (GW) {
             if (half == 0) {
               if (storer) tma_store_wait_read<OS - 1>();
               mbar_wait(&bars[L::B_OFULL + ob], (i >> 1) & 1);
@@ -892,9 +903,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               o16[q][e] = y.x;
               o16[q][e + 1] = y.y;
             }
-            store_chunk16_bf16(sO, row, 2 * half + q, o16[q]);
+            if (LA2_WARP_STORE) store_chunk16_bf16_sw64(sO + (q4 * 2 + half) * 2048, lane, q, o16[q]);
+            else store_chunk16_bf16(sO, row, 2 * half + q, o16[q]);
           }
           fence_proxy_async_smem();
+          if (LA2_WARP_STORE) {
+            __syncwarp();
+            if (lane == 0) {
+              uint8_t* sW = sO + (q4 * 2 + half) * 2048;
+              const int c0 = slice * DVS + half * 32, r0 = blk * BT + q4 * 32;
+              if (p.accum) tma_reduce_add_3d(mo, sW, c0, r0, bh);
+              else tma_store_3d(mo, sW, c0, r0, bh);
+              tma_store_commit();
+            }
+          } else {
           named_bar_sync(1 + q4, 64);
           if (storer) {
             if (p.accum)
@@ -906,10 +928,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_store_3d(mo, sO + q4 * 32 * 128, slice * DVS, blk * BT + q4 * 32, bh);
             tma_store_commit();
           }
+          }
           if (warp == LA2_TRW) TR(2, i, 6);
         }
       }
-      if (half == 0 && lane == 0) tma_store_wait_all0();
+      if ((LA2_WARP_STORE || half == 0) && lane == 0) tma_store_wait_all0();
     }
   } else if (warp < WY && !dqr) {
     // ------------------------------------------------------------- state warps
@@ -1211,10 +1234,10 @@ int tma_encoder_ready() { return get_encode(); }
 // Tensor maps depend only on (address, shape, box), so they are cached per host thread
 // (a map for the same address and shape is valid whatever tensor now lives there).
 static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows = BT,
-                     long long head_stride = 0, long long row_pitch = 0) {
+                     long long head_stride = 0, long long row_pitch = 0, int box_cols = 64) {
   struct Entry {
     const void* ptr;
-    int cols, N, BH, box;
+    int cols, N, BH, box, boxc;
     long long ld, rp;
     CUtensorMap map;
   };
@@ -1222,16 +1245,16 @@ static int make_tmap(CUtensorMap* m, const void* ptr, int cols, int N, int BH, i
   static thread_local int next = 0;
   for (const Entry& e : cache) {
     if (e.ptr == ptr && e.cols == cols && e.N == N && e.BH == BH && e.box == box_rows &&
-        e.ld == head_stride && e.rp == row_pitch && ptr) {
+        e.boxc == box_cols && e.ld == head_stride && e.rp == row_pitch && ptr) {
       *m = e.map;
       return 0;
     }
   }
-  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows, head_stride, row_pitch);
+  const int rc = make_tmap_bf16(m, ptr, cols, N, BH, box_rows, head_stride, row_pitch, box_cols);
   if (rc == 0) {
     Entry& e = cache[next];
     next = (next + 1) & 31;
-    e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.ld = head_stride;
+    e.ptr = ptr; e.cols = cols; e.N = N; e.BH = BH; e.box = box_rows; e.boxc = box_cols; e.ld = head_stride;
     e.rp = row_pitch;
     e.map = *m;
   }
@@ -1252,18 +1275,18 @@ static CUtensorMapL2promotion l2_promotion() {
   }
 }
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int box_rows,
-                   long long head_stride, long long row_pitch) {
+                   long long head_stride, long long row_pitch, int box_cols) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(N),
                         static_cast<cuuint64_t>(BH)};
   const cuuint64_t rp = row_pitch > 0 ? static_cast<cuuint64_t>(row_pitch) : static_cast<cuuint64_t>(cols);
   const cuuint64_t ld = head_stride > 0 ? static_cast<cuuint64_t>(head_stride)
                                         : rp * static_cast<cuuint64_t>(N);
   cuuint64_t strides[2] = {rp * 2, ld * 2};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                        box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -static_cast<int>(r) - 1000;
 }
@@ -1342,7 +1365,9 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     if (CM != 3 && (t == 5 || t == 6)) continue;
     const long long ld = (t < 4) ? a.ld[t] : (a1 ? a1->ld[t - 4] : a.ld[t - 4]);
     const long long rp = (t < 4) ? a.rp[t] : (a1 ? a1->rp[t - 4] : a.rp[t - 4]);
-    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, (t == 3 || t == 7) ? 32 : BT, ld, rp);
+    const bool omap = (t == 3 || t == 7);  // output: 32-row boxes (32 columns with LA2_WARP_STORE)
+    const int rc = make_tmap(maps[t], ptrs[t], cols[t], a.N, BH, omap ? 32 : BT, ld, rp,
+                             (omap && LA2_WARP_STORE) ? 32 : 64);
     if (rc != 0) {
       char buf[256];
       std::snprintf(buf, sizeof(buf),
@@ -1360,7 +1385,7 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
     if (kvb == nullptr) return set_error(LA2_ERR_VALUE, "per-block state buffer is null");
     const int nblk = (a.N + BT - 1) / BT;
     int rc = make_tmap(&mv1, kvb, DK, nblk * DK, BH, DK);
-    if (rc == 0 && CM == 4) rc = make_tmap(&mk1, a2->o, DK, a.N, BH, 32);
+    if (rc == 0 && CM == 4) rc = make_tmap(&mk1, a2->o, DK, a.N, BH, 32, 0, 0, LA2_WARP_STORE ? 32 : 64);
     if (rc != 0) return set_error(LA2_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state blocks / dQ");
   }
   FParams p;

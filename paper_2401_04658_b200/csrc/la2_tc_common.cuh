@@ -122,6 +122,21 @@ __device__ __forceinline__ void store_chunk16_bf16_dup(uint8_t* region, uint32_t
     st_cluster_v4(remote + o, w);
   }
 }
+// Write 16 fp32 values as bf16 into logical chunks 2q, 2q+1 of one 64-byte SW64 row
+// (chunk' = chunk ^ ((row >> 1) & 3)).
+__device__ __forceinline__ void store_chunk16_bf16_sw64(uint8_t* region, int row, int q, const float* x) {
+  uint8_t* rp = region + row * 64;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = 2 * q + h;
+    uint4 w;
+    w.x = pack_bf16x2(x[8 * h + 0], x[8 * h + 1]);
+    w.y = pack_bf16x2(x[8 * h + 2], x[8 * h + 3]);
+    w.z = pack_bf16x2(x[8 * h + 4], x[8 * h + 5]);
+    w.w = pack_bf16x2(x[8 * h + 6], x[8 * h + 7]);
+    *reinterpret_cast<uint4*>(rp + ((c ^ ((row >> 1) & 3)) * 16)) = w;
+  }
+}
 // Write 16 fp32 values as bf16 into logical chunks 2q, 2q+1 of one SW128 row.
 __device__ __forceinline__ void store_chunk16_bf16(uint8_t* region, int row, int q, const float* x) {
   uint8_t* rp = region + row * 128;
