@@ -63,26 +63,6 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #endif
 // how the peer gets its half of the operand: st.async per 16 bytes (0) or one bulk copy
 // per warp through the TMA unit (1)
-// d = 64 with O in the upper half of its S buffer too (O and Oe double-buffered; S reuse
-// then waits for the epilogue instead of PV)
-#ifndef LA2_OIS64
-#define LA2_OIS64 0
-#endif
-// d = 64 in-order X issuer: probe whether block i+1 has landed before issuing S_{i+1}, and
-// issue PV_i first if it has not
-#ifndef LA2_X_OPPORTUNISTIC
-#define LA2_X_OPPORTUNISTIC 0
-#endif
-// X issuer at d = 64 as the event loop too (S_{i+1} and PV_i issued as each becomes
-// ready) instead of the in-order S_{i+1}, PV_i, which makes PV_i wait for block i+1 to land
-#ifndef LA2_X_EVENT64
-#define LA2_X_EVENT64 0
-#endif
-// Y issuer as an event loop (folds run up to two blocks ahead of the Oe products) or in
-// program order (fold_i, Oe_i, fold_{i+1}, ...)
-#ifndef LA2_Y_EVENT
-#define LA2_Y_EVENT 0
-#endif
 #ifndef LA2_PEER_BULK
 #define LA2_PEER_BULK 0
 #endif
@@ -90,32 +70,18 @@ constexpr bool GW = (LA2_GROUP_WAIT != 0);
 #ifndef LA2_SO_NS
 #define LA2_SO_NS 4
 #endif
-// d = 128 full passes: Q/K and V in separate rings (2 and 3 deep, one V~ buffer) instead of
-// 2 stages of Q|K|V -- V is read last (PV needs the row warps' P), so a third V slot keeps
-// the next block's loads in flight while Q/K recycle as soon as S, the fold and Oe read them
-// d = 128 full passes: double-buffer the bf16 state operand (one V~ buffer pays for it),
-// so writing KV_i waits for Oe_{i-1} instead of Oe_i
-#ifndef LA2_KV2_128
-#define LA2_KV2_128 0
-#endif
 // Output epilogue: each row warp stages and TMA-stores its own [32 rows][32 cols] tile
 // (SW64, box 32 x 32) instead of the quarter's two warps meeting at two named barriers
 // around one [32][64] store
 #ifndef LA2_WARP_STORE
 #define LA2_WARP_STORE 1
 #endif
-#ifndef LA2_SPLIT_RING
-#define LA2_SPLIT_RING 0
-#endif
 
 template <int DK, bool SO, bool TRI = false>
 struct TcLayout {
   // Q/K/V stages; state-only passes stage only K and V (32 / 48 KB), so they get a deeper ring
   static constexpr int NS = SO ? LA2_SO_NS : ((DK == 64) ? 3 : 2);
-  static constexpr bool RING2 = (NS == 2) && !SO && (LA2_SPLIT_RING != 0);  // split Q/K | V rings
-  static constexpr int NSV = RING2 ? 3 : NS;      // V ring depth
-  static constexpr bool DBL128 = (DK == 128) && !SO && !RING2 && (LA2_KV2_128 != 0);
-  static constexpr int KTS = (RING2 || DBL128) ? 1 : 2;  // V~ buffers (scaled values)
+  static constexpr int KTS = 2;                   // V~ buffers (scaled values)
   // O staging buffers (the backward triple spends the second one on its state tiles)
   static constexpr int OS = (DK == 64 && !SO && !TRI) ? 2 : 1;
   static constexpr int Q_BYTES = SO ? 0 : BT * DK * 2;
@@ -127,12 +93,12 @@ struct TcLayout {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
-  static constexpr int OFF_S = OFF_V + NSV * V_BYTES;
+  static constexpr int OFF_S = OFF_V + NS * V_BYTES;
   static constexpr int OFF_KT = OFF_S + NS * S_BYTES;
   static constexpr int OFF_KV = OFF_KT + KTS * V_BYTES;
   // second bf16 state-operand buffer of the backward pair / triple's shared recurrence
   // (LA2_SPLIT_STATE): the triple's ranks 0-1 use their (otherwise idle) state-tile ring
-  static constexpr bool KV2 = ((DK == 64) && !SO && !TRI) || DBL128;
+  static constexpr bool KV2 = (DK == 64) && !SO && !TRI;
   static constexpr int OFF_O = OFF_KV + (KV2 ? 2 : 1) * KV_BYTES;
   static constexpr int OFF_KV2 = TRI ? OFF_S : OFF_KV + KV_BYTES;
   static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
@@ -140,14 +106,13 @@ struct TcLayout {
   static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
   static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
   static constexpr uint32_t STAGE_TX = Q_BYTES + K_BYTES + V_BYTES;
-  static constexpr uint32_t QK_TX = Q_BYTES + K_BYTES;  // RING2: the Q/K ring's share
   // TMEM columns. OIS ("O in S", d = 128): S[b] @128b holds the scores, then P (packed
   // bf16, cols +0..63) and O_i = P_i V_i (fp32, cols +64..127), so O is double-buffered
   // with S and PV_i does not wait for the epilogue of block i-1 | Oe[2] @256,320 |
   // dKV[2] @384,448. Otherwise (d = 64): S[2] @0,128 (P in cols +0..31, +64..95) | O @256
   // | Oe @320 | dKV[2] @384,448 -- S_{i+2} then only waits for PV_i, not for the epilogue.
   // State-only: dKV[2] @0,64.
-  static constexpr bool OIS = (DK == 128) || (LA2_OIS64 != 0);
+  static constexpr bool OIS = (DK == 128);
   // d = 128 (full passes): the V~ copy runs on its own warp, overlapping the state update
   // (-10 % at C3). d = 64 keeps it in the state warps: there the kernel is close to
   // issue-bound and a 16th busy warp slows its sub-partition (+8 %). State-only passes
@@ -157,9 +122,7 @@ struct TcLayout {
   static constexpr uint32_t TMEM_COLS = SO ? 128 : 512;
   static constexpr uint32_t T_O = 256, T_OE = OIS ? 256 : 320, T_KV = SO ? 0 : 384;
   // barrier slots
-  // (RING2: B_FULL / B_EMPTY guard the Q/K ring, B_FULLV / B_EMPTYV the V ring)
-  static constexpr int B_FULL = 0, B_EMPTY = NS, B_FULLV = 2 * NS, B_EMPTYV = B_FULLV + NSV,
-                       B_SFULL = B_EMPTYV + NSV, B_SFREE = B_SFULL + 2,
+  static constexpr int B_FULL = 0, B_EMPTY = NS, B_SFULL = 2 * NS, B_SFREE = B_SFULL + 2,
                        B_PREADY = B_SFREE + 2, B_OFULL = B_PREADY + 2, B_OEFULL = B_OFULL + 2,
                        B_OEMPTY = B_OEFULL + 2, B_KTREADY = B_OEMPTY + 2, B_KTFREE = B_KTREADY + KTS,
                        B_DKVFULL = B_KTFREE + KTS, B_DKVEMPTY = B_DKVFULL + 2,
@@ -251,12 +214,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
-    if (L::RING2) {
-      for (int s = 0; s < L::NSV; ++s) {
-        mbar_init(&bars[L::B_FULLV + s], 1);
-        mbar_init(&bars[L::B_EMPTYV + s], 2);  // X after PV, Y after the fold (V~ copy done); local
-      }
-    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[L::B_FULL + s], 1);
       // X after PV, Y after Oe (x2 in a cluster: the stage is shared)
@@ -312,7 +269,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // With a 2-stage ring (d = 128: 80 KB stages) a stage is refilled only one block
       // ahead, which exposes HBM latency; pull the next PF blocks into L2 so the ring's
       // TMA loads hit L2.
-      const int PF = (NS == 2 && !L::RING2) ? p.pf : 0;
+      const int PF = (NS == 2) ? p.pf : 0;
       const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
       auto tma_prefetch_l2_3d = [&](const CUtensorMap* m, int c0, int c1, int c2) {
         if (p.hint & 2) la2::tma_prefetch_l2_3d_hint(m, c0, c1, c2, pol_last);
@@ -380,29 +337,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      ((w.pos == nblk - 1 || g == sch.npre - 1) ? REC_SEG_END : 0);
           recs[g & 7] = rc;
         }
-        mbar_arrive_expect_tx(&bars[L::B_FULL + s],
-                              L::RING2 ? L::QK_TX : (dqr ? L::STAGE_TX + L::S_BYTES : L::STAGE_TX));
+        mbar_arrive_expect_tx(&bars[L::B_FULL + s], dqr ? L::STAGE_TX + L::S_BYTES : L::STAGE_TX);
         const int row = blk * BT;
         uint64_t* fb = &bars[L::B_FULL + s];
         uint8_t* dq = smem + L::OFF_Q + s * L::Q_BYTES;
         uint8_t* dk = smem + L::OFF_K + s * L::K_BYTES;   // stage region "K" (tile of tm_k)
         uint8_t* dv = smem + L::OFF_V + s * L::V_BYTES;   // stage region "V" (tile of tm_v)
-        uint64_t* fbv = fb;                                // the V tile's barrier
-        if (L::RING2) {
-          // V ring: slot g % NSV, refilled once X's PV and Y's fold of block g - NSV are done
-          const int sv = g % L::NSV;
-          if (g >= L::NSV) mbar_wait(&bars[L::B_EMPTYV + sv], ((g / L::NSV) - 1) & 1);
-          fbv = &bars[L::B_FULLV + sv];
-          mbar_arrive_expect_tx(fbv, L::V_BYTES);
-          dv = smem + L::OFF_V + sv * L::V_BYTES;
-        }
         if (CM == 0) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
             if (!SO) tma_load_3d(dq + c * REGION, mq, fb, c * 64, row, bh);
             tma_load_3d(dk + c * REGION, &tm_k, fb, c * 64, row, bh);
           }
-          tma_load_3d(dv, &tm_v, fbv, slice * DVS, row, bh);
+          tma_load_3d(dv, &tm_v, fb, slice * DVS, row, bh);
         } else if (CM == 1 || CM == 3) {
 #pragma unroll
           for (int c = 0; c < DK / 64; ++c) {
@@ -412,7 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_3d_mc(dk + c * REGION, mk, fb, c * 64, row, bh, mcmask);
             }
           }
-          tma_load_3d(dv, mv, fbv, slice * DVS, row, bh);
+          tma_load_3d(dv, mv, fb, slice * DVS, row, bh);
         } else if (CM == 2) {
           tma_load_3d(dq, mq, fb, 0, row, bh);  // own q: K (rank 0) or V (rank 1)
           if (crank == 0) tma_load_3d_mc(dk, &tm_k, fb, 0, row, bh, 0x3);  // Q -> region K
@@ -466,15 +413,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // and the O accumulator free) are issued as soon as each is ready, so PV_i never
       // waits behind the arrival of block i+1 -- that coupling would keep only one stage
       // load in flight with a 2-stage ring. S runs at most one block ahead of PV.
-      if (!SO && NS >= 3 && !LA2_X_EVENT64) {
+      if (!SO && NS >= 3) {
         // deep ring (d = 64): block i+1 has normally landed before PV_i is due, so the
         // plain order S_{i+1}, PV_i keeps the tensor pipe fed with the least polling
-        auto issue_S = [&](int j, bool ready = false) {
+        auto issue_S = [&](int j) {
           const int s = j % NS, b = j & 1;
-          if (!ready) {
-            mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
-            if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
-          }
+          mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+          if (j >= 2) mbar_wait(&bars[L::B_SFREE + b], ((j >> 1) - 1) & 1);
           tc_fence_after();
           if (leader) {
             const uint64_t q = adv(dQ0, s * L::Q_BYTES), k = adv(dK0, s * L::K_BYTES);
@@ -492,23 +437,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int s = i % NS, b = i & 1;
           const uint64_t v = adv(dV0, s * L::V_BYTES);
           TR(1, i, 0);
-          // S_{i+1} first when block i+1 has landed; otherwise PV_i first (one probe, no
-          // spinning), so PV_i -- and the stage release behind it -- never waits for a load
-          bool s_next = (i + 1 >= T);
-          if (!s_next && LA2_X_OPPORTUNISTIC && !REV) {  // forward scans only: measured faster
-                                                          // there, slower for the reverse pair / triple
-            int ok = 0;
-            if (lane == 0)
-              ok = mbar_test(&bars[L::B_FULL + (i + 1) % NS], ((i + 1) / NS) & 1) &&
-                   (i + 1 < 2 || mbar_test(&bars[L::B_SFREE + ((i + 1) & 1)], (((i + 1) >> 1) - 1) & 1));
-            if (__shfl_sync(0xffffffffu, ok, 0)) {
-              issue_S(i + 1, true);
-              s_next = true;
-            }
-          } else if (!s_next) {
-            issue_S(i + 1);
-            s_next = true;
-          }
+          if (i + 1 < T) issue_S(i + 1);
           TR(1, i, 1);
           mbar_wait(&bars[L::B_PREADY + b], (i >> 1) & 1);
           TR(1, i, 2);
@@ -527,7 +456,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             commit_empty(s);
           }
           __syncwarp();
-          if (!s_next) issue_S(i + 1);
         }
       } else if (!SO) {
         int nS = 0, nP = 0;
@@ -539,8 +467,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      (nS < 2 || mbar_test(&bars[L::B_SFREE + (nS & 1)], ((nS >> 1) - 1) & 1));
             if (nP < nS)
               p_ok = mbar_test(&bars[L::B_PREADY + (nP & 1)], (nP >> 1) & 1) &&
-                     (L::OIS || nP == 0 || mbar_test(&bars[L::B_OEMPTY + ((nP - 1) & 1)], ((nP - 1) >> 1) & 1)) &&
-                     (!L::RING2 || mbar_test(&bars[L::B_FULLV + nP % L::NSV], (nP / L::NSV) & 1));
+                     (L::OIS || nP == 0 || mbar_test(&bars[L::B_OEMPTY + ((nP - 1) & 1)], ((nP - 1) >> 1) & 1));
           }
           s_ok = __shfl_sync(0xffffffffu, s_ok, 0);
           p_ok = __shfl_sync(0xffffffffu, p_ok, 0);
@@ -560,13 +487,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 umma_bf16_ss(tbase + b * 128, adv(q, off), adv(k, off), ID_S, kk > 0);
               }
               umma_commit(&bars[L::B_SFULL + b]);
-              if (L::RING2) commit_empty(s);  // X's last read of the Q/K slot
             }
             ++nS;
           }
           if (p_ok) {
             const int s = nP % NS, b = nP & 1;
-            const uint64_t v = adv(dV0, (L::RING2 ? nP % L::NSV : s) * L::V_BYTES);
+            const uint64_t v = adv(dV0, s * L::V_BYTES);
             TR(1, nP, 3);
             if (leader) {
 #pragma unroll
@@ -577,8 +503,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               }
               if (!L::OIS) umma_commit(&bars[L::B_SFREE + b]);
               umma_commit(&bars[L::B_OFULL + b]);
-              if (L::RING2) umma_commit(&bars[L::B_EMPTYV + nP % L::NSV]);  // the V slot
-              else commit_empty(s);
+              commit_empty(s);
             }
             ++nP;
           }
@@ -602,8 +527,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma_commit(&bars[L::B_DKVFULL + db]);
           umma_commit(&bars[L::B_KTFREE + kt]);
           if (SO) commit_empty(s);
-          // the V~ copy of block i (done before KTREADY) was the V slot's other reader
-          if (L::RING2) umma_commit(&bars[L::B_EMPTYV + i % L::NSV]);
         }
         __syncwarp();
       };
@@ -633,8 +556,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                adv(dk, (kk >> 1) * 4096 + (kk & 1) * 32), ID_OS, kk > 0);
               }
             } else {
-              const uint64_t kvd = (L::DBL128 && (i & 1)) ? sdesc_sw128(smem_u32(smem + L::OFF_KV2), DK * 128, 1024)
-                                                           : dKV0;
+              const uint64_t kvd = dKV0;
 #pragma unroll
               for (int kk = 0; kk < DK / 16; ++kk)
                 umma_bf16_ss(tOE + (L::OIS ? db * 64 : 0), adv(q, (kk >> 2) * REGION + (kk & 3) * 32),
@@ -666,7 +588,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           __syncwarp();
           continue;
         }
-        if (!SO && LA2_Y_EVENT) break;  // the event loop below
         mbar_wait(&bars[L::B_KTREADY + kt], (i / KTS) & 1);
         if (i >= 2) mbar_wait(&bars[L::B_DKVEMPTY + db], ((i >> 1) - 1) & 1);
         mbar_wait(&bars[L::B_FULL + s], (i / NS) & 1);  // V visibility for this thread
@@ -675,7 +596,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (!SO) {
           // SPLIT: KV_{i-1} sits in operand buffer i & 1, half of it written by the peer
           if (SPLIT) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
-          else if (L::DBL128) mbar_wait(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1);
           else mbar_wait(&bars[L::B_KVREADY], i & 1);
           if (L::OIS && i >= 2) mbar_wait(&bars[L::B_OEMPTY + db], ((i >> 1) - 1) & 1);
           if (!L::OIS && i >= 1) mbar_wait(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
@@ -683,48 +603,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           issue_oe(i);
         }
         TR(1, i, 6);
-      }
-      if (!SO && !dqr && LA2_Y_EVENT) {
-        // Event loop: the fold of block i+1 (inputs: V~_{i+1}, a free dKV buffer) does not
-        // wait behind Oe_i (input: the state KV_{i-1}), so KV_{i+1} never waits for KV_{i-1}
-        // via this warp's issue order -- in order, the recurrence advanced one block per
-        // (fold latency + state update) and set the block period.
-        auto fold_ready = [&](int i) {
-          return mbar_test(&bars[L::B_KTREADY + i % KTS], (i / KTS) & 1) &&
-                 (i < 2 || mbar_test(&bars[L::B_DKVEMPTY + (i & 1)], ((i >> 1) - 1) & 1)) &&
-                 mbar_test(&bars[L::B_FULL + i % NS], (i / NS) & 1);
-        };
-        auto oe_ready = [&](int i) {
-          bool ok = SPLIT ? mbar_test(&bars[L::B_KVREADY + (i & 1)], (i >> 1) & 1)
-                          : mbar_test(&bars[L::B_KVREADY], i & 1);
-          if (L::OIS && i >= 2) ok = ok && mbar_test(&bars[L::B_OEMPTY + (i & 1)], ((i >> 1) - 1) & 1);
-          if (!L::OIS && i >= 1) ok = ok && mbar_test(&bars[L::B_OEMPTY + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
-          return ok;
-        };
-        int nF = 0, nO = 0;
-        while (nO < T) {
-          int f_ok = 0, o_ok = 0;
-          if (lane == 0) {
-            if (nF < T && nF < nO + 2) f_ok = fold_ready(nF) ? 1 : 0;
-            if (nO < nF) o_ok = oe_ready(nO) ? 1 : 0;
-          }
-          f_ok = __shfl_sync(0xffffffffu, f_ok, 0);
-          o_ok = __shfl_sync(0xffffffffu, o_ok, 0);
-          if (!f_ok && !o_ok) {
-            __nanosleep(20);
-            continue;
-          }
-          if (o_ok) {  // the older block first: Oe is on the output path
-            TR(1, nO, 4);
-            issue_oe(nO);
-            ++nO;
-          }
-          if (f_ok) {
-            TR(1, nF, 5);
-            issue_fold(nF);
-            ++nF;
-          }
-        }
       }
       // SPLIT: the last Oe's commits (ours and the peer's) have landed in this CTA's
       // KVFREE barrier before teardown (no tcgen05 arrive may target an exited CTA)
@@ -1081,14 +959,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           else mbar_arrive(&bars[L::B_KVREADY + b]);
         }
       } else {
-        uint8_t* dst = (L::DBL128 && b) ? smem + L::OFF_KV2 : sKVb;
+        uint8_t* dst = sKVb;
         if (has_kv) {
 #pragma unroll
           for (int q = 0; q < DVS / 16; ++q) store_chunk16_bf16(dst, kvrow, q, kv + 16 * q);
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[L::B_KVREADY + (L::DBL128 ? b : 0)]);
+        if (lane == 0) mbar_arrive(&bars[L::B_KVREADY]);
       }
     };
     if (!SO) {
@@ -1167,9 +1045,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (SPLIT) {
             if (i >= 1) mbar_wait(&bars[L::B_KVFREE + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
           }
-          else if (L::DBL128) {  // buffer (i + 1) & 1 was last read by Oe_{i-1}
-            if (i >= 1) mbar_wait(&bars[L::B_OEFULL + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
-          } else if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
+          else if (!GW || warp == W0) mbar_wait(&bars[L::B_OEFULL + (i & 1)], (i >> 1) & 1);
           if (GW) named_bar_sync(5, 128);
           if (st_states) {  // the previous block's state store has read the operand buffer
             if (warp == W0 && lane == 0) tma_store_wait_read<0>();
@@ -1190,10 +1066,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // V~_j = c . V_j (c_t = lam^(r-1-t), rev: lam^(t+1)), the fold operand of dKV_j. Off
     // the state warps, whose state update of block j-1 then overlaps this copy.
     for (int j = 0; j < T; ++j) {
-      // (RING2: the V slot of block j has its own barrier; it is published after the record)
-      const int s = L::RING2 ? j % L::NSV : j % NS, kt = j % KTS;
-      if (L::RING2) mbar_wait(&bars[L::B_FULLV + s], (j / L::NSV) & 1);
-      else mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
+      const int s = j % NS, kt = j % KTS;
+      mbar_wait(&bars[L::B_FULL + s], (j / NS) & 1);
       const BlkRec rc = recs[j & 7];
       const int r = min(BT, N - rc.blk * BT);
       if (j >= KTS) mbar_wait(&bars[L::B_KTFREE + kt], ((j / KTS) - 1) & 1);
