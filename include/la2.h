@@ -216,6 +216,27 @@ LA2_API int la2_decode_step_f64(const double* q, const double* k, const double* 
 LA2_API int la2_check_decay_f64(const double* decay, int H, void* stream);
 
 /*
+ * Norm(.) of NormAttention, O = Norm(Q (K^T V)) -- an extension: the
+ * reference leaves the normalisation out. Simple RMS normalisation of the
+ * attention-output rows, y = x / sqrt(mean(x^2) + eps), over the dv features of each head
+ * (group = 1) or over all H heads' features of a token (group = H: TransNormerLLM's SRMSNorm
+ * over the concatenated heads). rstd (fp32, [B,H,N] for group 1, [B,N] for group H) keeps
+ * 1 / sqrt(mean + eps) for the backward dx = (dy - y mean(dy y)) rstd.
+ *   la2_forward_norm      la2_forward (or la2_forward_states when kv_blocks != NULL) with the
+ *                         norm applied to o; fused into the tensor-core epilogue for bf16
+ *                         per-head norms with d <= 64, dv = 64, else a separate pass in place
+ *   la2_rmsnorm_forward   the norm alone (y may alias x)
+ *   la2_rmsnorm_backward  its backward from y and rstd
+ */
+LA2_API int la2_forward_norm(const void* q, const void* k, const void* v, const float* decay, void* o,
+                             const float* kv_in, float* kv_out, void* kv_blocks, float* rstd, float eps,
+                             int group, int B, int H, int N, int d, int dv, int dtype, void* stream);
+LA2_API int la2_rmsnorm_forward(const void* x, void* y, float* rstd, int B, int H, int N, int dv, int group,
+                                float eps, int dtype, void* stream);
+LA2_API int la2_rmsnorm_backward(const void* dy, const void* y, const float* rstd, void* dx, int B, int H,
+                                 int N, int dv, int group, int dtype, void* stream);
+
+/*
  * Scheduling knobs of the tensor-core kernels (process-wide; not a reference
  * interface). Results do not depend on them: the persistent schedule hands the fp32
  * state between work ranges exactly, so outputs are bitwise identical either way.

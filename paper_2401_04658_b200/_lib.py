@@ -54,6 +54,10 @@ SIGNATURES: dict[str, list] = {
     "la2_backward_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_decode_step_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "la2_check_decay_f64": [_vp, _i, _vp],
+    "la2_forward_norm": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_float, _i, _i, _i, _i, _i, _i,
+                         _i, _vp],
+    "la2_rmsnorm_forward": [_vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.c_float, _i, _vp],
+    "la2_rmsnorm_backward": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_launch_log": [_i],
     "la2_launch_log_read": [ctypes.POINTER(LaunchRecord), _i],
     "la2_set_tuning": [_i, _i],

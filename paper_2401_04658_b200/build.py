@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libla2.so"
-SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_simt.cu", "la2_f64.cu"]
+SOURCES = ["la2_api.cu", "la2_tc.cu", "la2_simt.cu", "la2_f64.cu", "la2_norm.cu"]
 # development library (include/la2_dev.h): operand-layout self-test and micro-benchmarks
 DEV_LIB = PKG / "libla2_dev.so"
 DEV_SOURCES = ["la2_selftest.cu"]

@@ -476,6 +476,58 @@ int la2_forward_states(const void* q, const void* k, const void* v, const float*
   return launch_tc(a, static_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- Norm(.) (la2_norm.cu)
+static int check_norm(int B, int H, int N, int dv, int group, int dtype) {
+  if (B < 1 || H < 1 || N < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad shape");
+  if (dv > 1024) return set_error(LA2_ERR_UNSUPPORTED, "norm rows must have dv <= 1024");
+  if (group != 1 && group != H) return set_error(LA2_ERR_VALUE, "norm group must be 1 (per head) or H (all heads)");
+  if (dtype != LA2_BF16 && dtype != LA2_FP32) return set_error(LA2_ERR_UNSUPPORTED, "dtype must be LA2_BF16 or LA2_FP32");
+  return 0;
+}
+
+int la2_rmsnorm_forward(const void* x, void* y, float* rstd, int B, int H, int N, int dv, int group, float eps,
+                        int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_norm(B, H, N, dv, group, dtype)) return rc;
+  if (!x || !y || !rstd) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (!(eps > 0.f)) return set_error(LA2_ERR_VALUE, "eps must be > 0");
+  if (int rc = bind_device(stream, x)) return rc;
+  return launch_rmsnorm_fwd(x, y, rstd, B, H, N, dv, group, eps, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int la2_rmsnorm_backward(const void* dy, const void* y, const float* rstd, void* dx, int B, int H, int N, int dv,
+                         int group, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_norm(B, H, N, dv, group, dtype)) return rc;
+  if (!dy || !y || !rstd || !dx) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (int rc = bind_device(stream, dy)) return rc;
+  return launch_rmsnorm_bwd(dy, y, rstd, dx, B, H, N, dv, group, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int la2_forward_norm(const void* q, const void* k, const void* v, const float* decay, void* o,
+                     const float* kv_in, float* kv_out, void* kv_blocks, float* rstd, float eps, int group,
+                     int B, int H, int N, int d, int dv, int dtype, void* stream) {
+  g_err[0] = 0;
+  if (int rc = check_common(B, H, N, d, dv, dtype, decay)) return rc;
+  if (int rc = check_norm(B, H, N, dv, group, dtype)) return rc;
+  if (!q || !k || !v || !o || !rstd) return set_error(LA2_ERR_VALUE, "null tensor pointer");
+  if (!(eps > 0.f)) return set_error(LA2_ERR_VALUE, "eps must be > 0");
+  if (kv_blocks != nullptr && !states_eligible(dtype, d, dv))
+    return set_error(LA2_ERR_UNSUPPORTED, "stored per-block states need bf16 with d = dv = 64");
+  if (int rc = bind_device(stream, q)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FArgs a{q, k, v, o, decay, kv_in, 0, kv_out, B, H, N, d, dv, dtype, 0};
+  a.kv_blocks = kv_blocks;
+  // per-head norm of a d <= 64, dv = 64 bf16 forward: fused into the tensor-core epilogue
+  if (group == 1 && tc_eligible(dtype, d, dv) && d <= 64 && dv == 64) {
+    a.norm_eps = eps;
+    a.rstd = rstd;
+    return launch_tc(a, st);
+  }
+  if (int rc = (kv_blocks != nullptr) ? launch_tc(a, st) : run_f(a, st)) return rc;
+  return launch_rmsnorm_fwd(o, o, rstd, B, H, N, dv, group, eps, dtype, st);
+}
+
 int la2_backward_states(const void* q, const void* k, const void* v, const void* dout,
                         const float* decay, const void* kv_blocks, void* dq, void* dk, void* dv,
                         const float* dkv_in, float* dkv_out, int B, int H, int N, int d, int dvd,

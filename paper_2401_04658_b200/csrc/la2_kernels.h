@@ -47,6 +47,9 @@ struct FArgs {
   // per-block bf16 states [B*H][ceil(N/128)][dk][dv] (d = dv = 64): written by a forward
   // (store), read by the backward triple's dQ CTA
   void* kv_blocks = nullptr;
+  // per-head RMS norm of the output rows fused into the epilogue (la2_forward_norm)
+  float norm_eps = 0.f;
+  float* rstd = nullptr;
 };
 
 // Kernel-side parameter block (passed by value).
@@ -70,6 +73,8 @@ struct FParams {
   int accum;  // output epilogue: TMA reduce-add into o
   int store_states;  // forward (d = 64): write the per-block bf16 states through tm_v1
   int dkr;           // real head dim of the pass (<= the kernel's DK; rows beyond it are padding)
+  float norm_eps;    // > 0: per-head RMS norm fused into the output epilogue (d = dv = 64 forward)
+  float* rstd;       //   its per-row 1 / rms, [B*H][N]
 };
 
 int launch_tc(const FArgs& a, cudaStream_t st);
@@ -93,6 +98,12 @@ int launch_f64(const double* q, const double* k, const double* v, double* o, con
                int reverse, int block, cudaStream_t st);
 int launch_decode_f64(const double* q, const double* k, const double* v, const double* decay,
                       double* state, double* o, int B, int H, int d, int dv, cudaStream_t st);
+// Norm(.) of NormAttention (la2_norm.cu): rows of [B,H,N,dv] normalised per head
+// (group = 1) or over all heads of a token (group = H); rstd [B*H/group*N]
+int launch_rmsnorm_fwd(const void* x, void* y, float* rstd, int B, int H, int N, int dv, int group, float eps,
+                       int dtype, cudaStream_t st);
+int launch_rmsnorm_bwd(const void* dy, const void* y, const float* rstd, void* dx, int B, int H, int N, int dv,
+                       int group, int dtype, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
                   void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);
 int launch_state_scan(const float* chunk_states, const float* decay, const float* init,

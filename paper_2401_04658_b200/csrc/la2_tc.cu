@@ -101,7 +101,11 @@ struct TcLayout {
   static constexpr bool KV2 = (DK == 64) && !SO && !TRI;
   static constexpr int OFF_O = OFF_KV + (KV2 ? 2 : 1) * KV_BYTES;
   static constexpr int OFF_KV2 = TRI ? OFF_S : OFF_KV + KV_BYTES;
-  static constexpr int OFF_BAR = OFF_O + OS * O_BYTES;
+  // fused per-head RMS norm (d = dv = 64 forward): each quarter's two row warps exchange
+  // their half-row sums of squares through [2][128] floats
+  static constexpr int NORM_BYTES = (DK == 64 && !SO && !TRI) ? 1024 : 0;
+  static constexpr int OFF_NORM = OFF_O + OS * O_BYTES;
+  static constexpr int OFF_BAR = OFF_NORM + NORM_BYTES;
   static constexpr int BAR_BYTES = 512;
   static constexpr int OFF_REC = OFF_BAR + BAR_BYTES;  // per-block schedule records (ring of 8)
   static constexpr int TOTAL = OFF_REC + 8 * 32 + 1024;  // + alignment slack
@@ -182,6 +186,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // shared recurrence of the backward pair / triple (LA2_SPLIT_STATE): ranks 0-1 fold
   // Q^T (c . dO) (Q at OFF_K, dO at OFF_V in both), columns [32 crank, 32 crank + 32)
   constexpr bool SPLIT = (CM == 2 || CM == 4) && (LA2_SPLIT_STATE != 0);
+  constexpr bool NORM_OK = (DK == 64) && !REV && !SO && (CM == 0);  // fused Norm(.) epilogue
   constexpr int KVC = SPLIT ? 32 : DVS;               // state columns held by this CTA
   const int kc0 = SPLIT ? 32 * static_cast<int>(crank) : 0;
   const CUtensorMap* mq = (sib || dqr) ? &tm_q1 : &tm_q;  // dqr: its own copy of V (tm_q1)
@@ -781,6 +786,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               o16[q][e] = y.x;
               o16[q][e + 1] = y.y;
             }
+          }
+          if (NORM_OK && p.norm_eps > 0.f) {
+            // Norm(.): y = o / sqrt(mean(o^2) + eps) over the row's 64 values, split over this
+            // quarter's two warps (32 each): exchange the half sums through smem
+            float ss = 0.f;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+              for (int e = 0; e < 16; ++e) ss = fmaf(o16[q][e], o16[q][e], ss);
+            float* sn = reinterpret_cast<float*>(smem + L::OFF_NORM);
+            sn[half * 128 + row] = ss;
+            named_bar_sync(1 + q4, 64);
+            const float rs = rsqrtf((ss + sn[(1 - half) * 128 + row]) * (1.f / 64.f) + p.norm_eps);
+            named_bar_sync(1 + q4, 64);  // both read before the next block overwrites
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o16[q][e] *= rs;
+            if (half == 0 && blk * BT + row < N) p.rstd[static_cast<size_t>(bh) * N + blk * BT + row] = rs;
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
             if (LA2_WARP_STORE) store_chunk16_bf16_sw64(sO + (q4 * 2 + half) * 2048, lane, q, o16[q]);
             else store_chunk16_bf16(sO, row, 2 * half + q, o16[q]);
           }
@@ -1284,6 +1311,14 @@ static int launch_tc_t(const FArgs& a, cudaStream_t st, const FArgs* a1 = nullpt
   constexpr int CS = (CM == 3) ? 4 : ((CM == 4) ? 3 : (CM ? 2 : 1));
   p.nsl = (a.dv + DVS - 1) / DVS;
   p.dkr = a.dk;
+  p.norm_eps = 0.f;
+  p.rstd = nullptr;
+  if (a.norm_eps > 0.f) {
+    if (!(DK == 64 && !REV && !SO && CM == 0 && a.dv == DVS && a.rstd != nullptr))
+      return set_error(LA2_ERR_UNSUPPORTED, "the fused norm epilogue needs a d <= 64, dv = 64 forward");
+    p.norm_eps = a.norm_eps;
+    p.rstd = a.rstd;
+  }
   p.units = (CM == 2 || CM == 4) ? BH : ((CM == 1 || CM == 3) ? BH * p.nsl / 2 : BH * p.nsl);
   p.P = p.units;
   p.ws = nullptr;

@@ -351,6 +351,64 @@ def la2_backward_states(q, k, v, d_out, decay: DecayLike, kv_blocks: torch.Tenso
     return dq, dk, dvv, dkv_out
 
 
+# --------------------------------------------------------------------- Norm(.)
+def _norm_group(norm: str, H: int) -> int:
+    if norm == "head":
+        return 1
+    if norm == "heads":
+        return H
+    raise ValueError(f"norm must be None, 'head' (per head) or 'heads' (over all heads), got {norm!r}")
+
+
+def rmsnorm_forward(x: torch.Tensor, eps: float = 1e-6, norm: str = "head", out: Optional[torch.Tensor] = None):
+    """Norm(.) of NormAttention (an extension, SPEC.md:167 leaves it out):
+    y = x / sqrt(mean(x^2) + eps) over each head's dv features ("head") or over all heads'
+    features of a token ("heads"). Returns ``(y, rstd)``; ``out=x`` normalises in place."""
+    B, H, N, dv = x.shape
+    grp = _norm_group(norm, H)
+    x = x.contiguous()
+    y = torch.empty_like(x) if out is None else out
+    rstd = torch.empty(B, H // grp, N, device=x.device, dtype=torch.float32)
+    _lib.call("la2_rmsnorm_forward", _ptr(x), _ptr(y), _ptr(rstd), B, H, N, dv, grp, float(eps), _code(x),
+              _stream(x.device))
+    return y, rstd
+
+
+def rmsnorm_backward(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor, norm: str = "head") -> torch.Tensor:
+    """dx = (dy - y mean(dy y)) rstd, the backward of :func:`rmsnorm_forward`."""
+    B, H, N, dv = y.shape
+    grp = _norm_group(norm, H)
+    dy = dy.to(y.dtype).contiguous()
+    dx = torch.empty_like(y)
+    _lib.call("la2_rmsnorm_backward", _ptr(dy), _ptr(y), _ptr(rstd), _ptr(dx), B, H, N, dv, grp, _code(y),
+              _stream(y.device))
+    return dx
+
+
+def la2_forward_norm(q, k, v, decay: DecayLike, eps: float = 1e-6, norm: str = "head",
+                     kv_in: Optional[torch.Tensor] = None, output_final_state: bool = False,
+                     store_states: bool = False):
+    """Forward with Norm(.) applied to the output (include/la2.h la2_forward_norm): fused into
+    the tensor-core epilogue for bf16 per-head norms with d <= 64, dv = 64. Returns
+    ``(y, rstd, kv_out, kv_blocks)``; kv_blocks (the per-block states for
+    :func:`la2_backward_states`) only with ``store_states``."""
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    if q.dtype == _F64:
+        raise ValueError("Norm(.) runs on bf16 / fp32 inputs")
+    grp = _norm_group(norm, H)
+    dec = _decay(decay, H, q.device)
+    kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in")
+    kv_out = torch.empty(B, H, d, dv, device=q.device, dtype=torch.float32) if output_final_state else None
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(v)
+    rstd = torch.empty(B, H // grp, N, device=q.device, dtype=torch.float32)
+    blocks = (torch.empty(B, H, (N + 127) // 128, d, dv, device=q.device, dtype=torch.bfloat16)
+              if store_states else None)
+    _lib.call("la2_forward_norm", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(o), _ptr(kv_in), _ptr(kv_out),
+              _ptr(blocks), _ptr(rstd), float(eps), grp, B, H, N, d, dv, _code(q), _stream(q.device))
+    return o, rstd, kv_out, blocks
+
+
 def _head_stride(t: torch.Tensor) -> Optional[int]:
     """Element stride between consecutive (b, h) rows of a [B,H,N,c] view whose rows are
     contiguous and evenly spaced (la2_forward_strided), else None."""
@@ -539,15 +597,26 @@ class LightningAttn2Fn(torch.autograd.Function):
     the reference's backward (pkg/src/tila/kernel.py:184-204)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, decay, initial_state, output_final_state, seq_split):
+    def forward(ctx, q, k, v, decay, initial_state, output_final_state, seq_split, norm=None, norm_eps=1e-6):
         B, H, N, d = q.shape
         g = split_factor(B, H, N, d, v.shape[3], q.dtype) if seq_split == "auto" else int(seq_split)
         ctx.stored = False
+        ctx.norm = norm
+        rstd = None
+        stored = (STORED_STATES and N >= STORED_STATES_MIN_N and states_eligible(q, v)
+                  and any(ctx.needs_input_grad[:3]))
         if g > 1:
             o, kv_out, prefix = split_forward(q, k, v, decay, g, kv_in=initial_state,
                                               output_final_state=output_final_state)
-        elif (STORED_STATES and N >= STORED_STATES_MIN_N and states_eligible(q, v)
-              and any(ctx.needs_input_grad[:3])):
+            if norm is not None:
+                o, rstd = rmsnorm_forward(o, norm_eps, norm, out=o)
+        elif norm is not None:
+            # Norm(.) fused into the epilogue where the kernel allows it (la2_forward_norm)
+            o, rstd, kv_out, prefix = la2_forward_norm(q, k, v, decay, norm_eps, norm, kv_in=initial_state,
+                                                       output_final_state=output_final_state,
+                                                       store_states=stored)
+            ctx.stored = stored
+        elif stored:
             # d = 64: keep the per-block states (half a tensor of HBM) so the backward's dQ
             # needs no replay scan and shares the dK / dV passes' reads
             o, kv_out, prefix = la2_forward_states(q, k, v, decay, kv_in=initial_state,
@@ -558,7 +627,7 @@ class LightningAttn2Fn(torch.autograd.Function):
                                     output_final_state=output_final_state)
             prefix = None
         ctx.g = g
-        ctx.save_for_backward(q, k, v, decay, initial_state, prefix)
+        ctx.save_for_backward(q, k, v, decay, initial_state, prefix, o if norm is not None else None, rstd)
         ctx.set_materialize_grads(False)
         ctx.want_state_grad = initial_state is not None and initial_state.requires_grad
         if kv_out is None:
@@ -567,10 +636,12 @@ class LightningAttn2Fn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, d_o, *rest):
-        q, k, v, decay, initial_state, prefix = ctx.saved_tensors
+        q, k, v, decay, initial_state, prefix, y, rstd = ctx.saved_tensors
         d_final = rest[0] if rest else None
         if d_o is None:
             d_o = torch.zeros_like(v)
+        elif ctx.norm is not None:
+            d_o = rmsnorm_backward(d_o, y, rstd, ctx.norm)  # through Norm(.) to the attention output
         if ctx.g > 1:
             dq, dk, dv, dkv = split_backward(q, k, v, d_o.to(q.dtype).contiguous(), decay, ctx.g, prefix,
                                              dkv_in=d_final, output_dkv=ctx.want_state_grad)
@@ -580,12 +651,12 @@ class LightningAttn2Fn(torch.autograd.Function):
         else:
             dq, dk, dv, dkv = la2_backward(q, k, v, d_o.to(q.dtype), decay, kv_in=initial_state,
                                            dkv_in=d_final, output_dkv=ctx.want_state_grad)
-        return dq, dk, dv, None, dkv, None, None
+        return dq, dk, dv, None, dkv, None, None, None, None
 
 
 def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: DecayLike,
                     initial_state: Optional[torch.Tensor] = None, output_final_state: bool = False,
-                    seq_split="auto"):
+                    seq_split="auto", norm: Optional[str] = None, norm_eps: float = 1e-6):
     """Causal linear attention with per-head exponential decay, on the GPU.
 
     Args:
@@ -596,6 +667,10 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
       output_final_state: also return the fp32 final state.
       seq_split: "auto" (split long sequences into chunks when B*H is too small to
         fill the GPU, see :func:`split_factor`) or an explicit chunk count (1 = off).
+      norm: None (the reference's semantics), or Norm(.) of NormAttention applied to the
+        output: "head" = RMS over each head's dv features (fused into the
+        tensor-core epilogue for bf16 d <= 64, dv = 64), "heads" = over all heads' features
+        of a token (TransNormerLLM's SRMSNorm); bf16 / fp32 only.
     Returns ``o`` (``[B,H,N,dv]``, input dtype), or ``(o, final_state)``.
     """
     _check_qkv(q, k, v)
@@ -607,4 +682,9 @@ def lightning_attn2(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, decay: De
             raise ValueError(f"initial_state must have shape {(B, H, d, v.shape[3])}")
         if initial_state.dtype != sdt:
             initial_state = initial_state.to(sdt)
-    return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state), seq_split)
+    if norm is not None:
+        _norm_group(norm, q.shape[1])
+        if q.dtype == _F64:
+            raise ValueError("Norm(.) runs on bf16 / fp32 inputs")
+    return LightningAttn2Fn.apply(q, k, v, dec, initial_state, bool(output_final_state), seq_split, norm,
+                                  float(norm_eps))

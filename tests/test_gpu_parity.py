@@ -1128,3 +1128,63 @@ def test_make_graphed_callables_fwd_bwd():
         outs.append([o.detach(), qg.grad, kg.grad, vg.grad])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------ Norm(.) extension
+def _np_norm(x, eps, group):
+    """y = x / sqrt(mean(x^2) + eps) per (b, h, t) row (group 1) or per (b, t) over all heads."""
+    if group == "head":
+        r = np.sqrt((x * x).mean(axis=-1, keepdims=True) + eps)
+    else:
+        r = np.sqrt((x * x).mean(axis=(1, 3), keepdims=True) + eps)
+    return x / r, r
+
+
+def _np_norm_bwd(dy, y, r, group):
+    if group == "head":
+        m = (dy * y).mean(axis=-1, keepdims=True)
+    else:
+        m = (dy * y).mean(axis=(1, 3), keepdims=True)
+    return (dy - y * m) / r
+
+
+@pytest.mark.parametrize("B,H,N,d,dv,norm", [(2, 3, 700, 64, 64, "head"), (2, 3, 300, 32, 64, "head"),
+                                             (1, 3, 500, 128, 128, "head"), (2, 4, 400, 64, 64, "heads"),
+                                             (1, 2, 16384, 64, 64, "head")])
+def test_norm_extension_against_oracle(B, H, N, d, dv, norm):
+    """Norm(.) of NormAttention, an extension beyond the reference
+    (SPEC.md:167): lightning_attn2(..., norm=) against the fp64 oracle followed by the same
+    normalisation, forward and gradients. d <= 64, dv = 64 per-head norms run fused into the
+    tensor-core epilogue (N = 16K: with the stored-state backward triple)."""
+    eps = 1e-6
+    decay = [0.9, 0.99, 0.999, 1.0][:H]
+    q, k, v, do = inputs(B, H, N, d, dv, torch.bfloat16, seed=N + d)
+    qg, kg, vg = (t.to(DEV).requires_grad_() for t in (q, k, v))
+    y = la2.lightning_attn2(qg, kg, vg, decay, norm=norm, norm_eps=eps)
+    y.backward(do.to(DEV))
+    Q, K, V, DO = (to64(t) for t in (q, k, v, do))
+    x = port.bhnd_forward(Q, K, V, decay, block=256)[0] if N > 4096 else port.bhnd_oracle_forward(Q, K, V, decay)
+    ry, r = _np_norm(x, eps, norm)
+    dx = _np_norm_bwd(DO, ry, r, norm)
+    if N > 4096:
+        rq, rk, rv = port.bhnd_backward(Q, K, V, dx, decay, block=256)
+    else:
+        rq, rk, rv = port.bhnd_oracle_backward(Q, K, V, dx, decay)
+    errs = {"y": rel(y, ry), "dq": rel(qg.grad, rq), "dk": rel(kg.grad, rk), "dv": rel(vg.grad, rv)}
+    print(B, H, N, d, dv, norm, errs)
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_norm_fused_matches_unfused():
+    """The fused epilogue norm (la2_forward_norm, d = dv = 64) against la2_forward followed by
+    the standalone rmsnorm kernel: same rows, the same rstd up to bf16 rounding of o."""
+    from paper_2401_04658_b200 import ops
+
+    B, H, N = 2, 4, 1000
+    q, k, v = gpu(*inputs(B, H, N, 64, 64, torch.bfloat16, seed=3)[:3])
+    decay = [0.5, 0.9, 0.99, 1.0]
+    y1, r1, _, _ = ops.la2_forward_norm(q, k, v, decay, 1e-6, "head")
+    o, _ = la2.la2_forward(q, k, v, decay)
+    y2, r2 = ops.rmsnorm_forward(o, 1e-6, "head")
+    assert (y1.float() - y2.float()).abs().max().item() <= 2e-2 * y2.float().abs().max().item()
+    assert torch.allclose(r1, r2, rtol=1e-2)

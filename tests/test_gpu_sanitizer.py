@@ -28,6 +28,9 @@ pytestmark = pytest.mark.gpu
     ("memcheck", "4,40,1000,64,s"),
     ("racecheck", "1,3,700,64,s"),
     ("synccheck", "1,3,700,64,s"),
+    # the fused Norm(.) epilogue (the two row warps of a quarter exchange row sums in smem)
+    ("racecheck", "1,3,700,64,n"),
+    ("memcheck", "2,40,700,64,n"),
 ])
 def test_sanitizer_clean(tool, shape):
     if not os.path.exists(SAN):

@@ -10,10 +10,15 @@ from paper_2401_04658_b200 import ops
 spec = sys.argv[1].split(',') if len(sys.argv) > 1 else ['8', '16', '16384', '64']
 B, H, N, D = map(int, spec[:4])
 stored = len(spec) > 4 and spec[4] == 's'
+normed = len(spec) > 4 and spec[4] == 'n'  # Norm(.) fused into the forward epilogue
 dev = torch.device('cuda', 0)
 q, k, v, do = ((torch.rand(B, H, N, D, device=dev) * 2 - 1).bfloat16() for _ in range(4))
 dec = la2.decay_tensor(alibi_decay(H), H, dev)
-if stored:
+if normed:
+    y, rstd, _, _ = ops.la2_forward_norm(q, k, v, dec, 1e-6, "head")
+    dx = ops.rmsnorm_backward(do, y, rstd, "head")
+    la2.la2_backward(q, k, v, dx, dec)
+elif stored:
     _, _, blocks = ops.la2_forward_states(q, k, v, dec)
     ops.la2_backward_states(q, k, v, do, dec, blocks)
 else:
