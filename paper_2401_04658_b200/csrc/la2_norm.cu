@@ -143,14 +143,13 @@ __global__ void __launch_bounds__(256)
     la2_rmsnorm_vec_kernel(const T* a, const T* b, T* out, float* rstd, int B, int H, int N, int dv, int group,
                            float eps) {
   constexpr int MAXC = 4;  // chunks per thread held in registers (rows of <= 4 * TPR * 8 elements)
-  const long long rows = static_cast<long long>(B) * (H / group) * N;
+  // grid: x = blocks of 256 / TPR tokens, y = (b, head group) -- no 64-bit divisions
   const int team = threadIdx.x / TPR, tl = threadIdx.x % TPR;
-  const long long row = static_cast<long long>(blockIdx.x) * (256 / TPR) + team;
-  const bool live = row < rows;
-  const long long rr = live ? row : 0;
-  const int t = static_cast<int>(rr % N);
-  const long long bg = rr / N;
-  const int hg = static_cast<int>(bg % (H / group)), bb = static_cast<int>(bg / (H / group));
+  const int t = blockIdx.x * (256 / TPR) + team;
+  const bool live = t < N;
+  const int bg = blockIdx.y;
+  const int hg = bg % (H / group), bb = bg / (H / group);
+  const long long rr = static_cast<long long>(bg) * N + (live ? t : 0);
   const int cps = dv / 8, nch = group * cps;  // chunks per segment / per row
   Vec8<T> va[MAXC], vb[MAXC];
   float acc = 0.f;
@@ -196,8 +195,8 @@ static bool launch_rmsnorm_vec(const void* a, const void* b, void* out, float* r
   int tpr = 1;
   while (tpr < 32 && tpr * 2 < nch) tpr *= 2;  // ~2 chunks (16 elements) per thread
   if (nch > 4 * tpr) return false;             // rows longer than 4 * 32 * 8 elements
-  const long long rows = static_cast<long long>(B) * (H / group) * N;
-  const unsigned blocks = static_cast<unsigned>((rows + 256 / tpr - 1) / (256 / tpr));
+  if (static_cast<long long>(B) * (H / group) > 65535) return false;
+  const dim3 blocks((N + 256 / tpr - 1) / (256 / tpr), B * (H / group));
   const T* ta = static_cast<const T*>(a);
   const T* tb = static_cast<const T*>(b);
   T* to = static_cast<T*>(out);
