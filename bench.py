@@ -574,8 +574,10 @@ def main():
     if not args.no_e2e:
         host = [t.cpu().pin_memory() for t in make(N, 7)]
         h2d = sum(t.numel() * t.element_size() for t in host)
-        outs = [[torch.empty_like(host[0]).pin_memory() for _ in range(4)] for _ in range(2)]
-        d2h = sum(t.numel() * t.element_size() for t in outs[0])
+        # one set of pinned result buffers (the downloads are ordered on one stream); two
+        # device input sets so step s+1's upload overlaps step s
+        outs = [torch.empty_like(host[0]).pin_memory() for _ in range(4)]
+        d2h = sum(t.numel() * t.element_size() for t in outs)
         dev_in = [[torch.empty_like(t, device=dev) for t in host] for _ in range(2)]
         s_up, s_down, s_comp = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.current_stream()
         ev_in = [torch.cuda.Event() for _ in range(2)]     # inputs of set b landed
@@ -604,7 +606,7 @@ def main():
                 ev_out[b].record(s_comp)
                 s_down.wait_event(ev_out[b])
                 with torch.cuda.stream(s_down):
-                    for dst, src in zip(outs[b], res):
+                    for dst, src in zip(outs, res):
                         src.record_stream(s_down)
                         dst.copy_(src, non_blocking=True)
             torch.cuda.synchronize()
@@ -625,7 +627,7 @@ def main():
                         f"({link:.0f} GB/s both directions together) vs {ms:.2f} ms of device time",
                "api": "paper_2401_04658_b200.lightning_attn2 autograd fwd+bwd; q,k,v,dO from pinned "
                       "host, o,dq,dk,dv back to pinned host; uploads / downloads on two copy streams "
-                      "overlapping the neighbouring steps (software pipeline, 2 buffer sets)"}
+                      "overlapping the neighbouring steps (software pipeline, 2 device input sets)"}
         del dev_in, outs, host
 
     # ---------------- CPU baseline (rank 0, N=1 only)
