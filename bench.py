@@ -784,6 +784,22 @@ def extra_workload(args, world, rank, local_rank):
                     "residency": "L2" if Bd * H * D * D * 4 < 100 * 2**20 else "HBM",
                     "frac_of_hbm": gbs / hbm_peak})
                 del st0, st, qd, kd, vd, graph
+            # Multi-token decode (la2_decode_tokens: T tokens per launch, state kept in
+            # registers across them): batch 256, the HBM-bound case, where the state
+            # crossing HBM once per T tokens is the gain
+            line["decode_multi"] = []
+            Bd = 256
+            st = torch.zeros(Bd, H, D, D, device=dev)
+            for T in (4, 8, 16):
+                qd, kd, vd = (rand((Bd, H, T, D), torch.bfloat16, 20 + i) for i in range(3))
+                ms_d = timed(lambda: la2.decode_tokens(qd, kd, vd, dec, st), max(3, args.steps // 4), 2)
+                nbytes = Bd * H * D * D * 4 * 2 + 4 * Bd * H * T * D * 2
+                line["decode_multi"].append({
+                    "batch": Bd, "tokens_per_launch": T, "us_per_launch": ms_d * 1e3,
+                    "tokens_per_s": Bd * T * world / (ms_d / 1e3),
+                    "gbs": nbytes / (ms_d / 1e3) / 1e9, "frac_of_hbm": nbytes / (ms_d / 1e3) / 1e9 / hbm_peak})
+                del qd, kd, vd
+            del st
     else:  # c5
         H, D, N_total = 16, 128, 524288
         L = N_total // world

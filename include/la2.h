@@ -188,6 +188,19 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
                     float* state, void* o, int B, int H, int d, int dv, int dtype, void* stream);
 
 /*
+ * T decode steps per (b, h) in one launch, in place on `state`: tila.inference_step folded
+ * over T tokens (reference.py:162-181), i.e. tila.recurrent_forward (reference.py:142-159)
+ * continued from `state` (a zeroed state gives recurrent_forward itself). Each token
+ * runs the single step's arithmetic in the same order, so the result equals T calls of
+ * la2_decode_step bit for bit; the state crosses HBM once per call instead of once per
+ * token (multi-token decode: speculative / chunked continuation of a stream).
+ * q,k: [B,H,T,d]  v,o: [B,H,T,dv]  state: [B,H,d,dv] fp32. T = 0 is a no-op.
+ */
+LA2_API int la2_decode_tokens(const void* q, const void* k, const void* v, const float* decay,
+                              float* state, void* o, int B, int H, int T, int d, int dv, int dtype,
+                              void* stream);
+
+/*
  * Double precision: the reference's default dtype (every tila routine computes in the
  * input dtype, np.result_type; pkg/src/tila/reference.py:54-74). fp64 storage and
  * arithmetic on the CUDA cores (DFMA), decay powers by iterated products flushed below
@@ -196,6 +209,7 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  *   la2_forward_f64      tila.tiled_forward / chunked_forward  (kernel.py:122-162)
  *   la2_backward_f64     tila.tiled_backward                  (kernel.py:165-233)
  *   la2_decode_step_f64  tila.inference_step                  (reference.py:162-181)
+ *   la2_decode_tokens_f64 tila.recurrent_forward / folded inference_step (reference.py:142-181)
  *   la2_check_decay_f64  the decay validation of reference.py:42-44
  * d, dv <= 256; no sequence split, no tensor cores: a correctness path for the tila
  * adapter (the reference's 1e-10 gates), not a throughput path. `block` is the
@@ -213,6 +227,9 @@ LA2_API int la2_backward_f64(const double* q, const double* k, const double* v, 
                              int N, int d, int dv_dim, int block, void* stream);
 LA2_API int la2_decode_step_f64(const double* q, const double* k, const double* v, const double* decay,
                                 double* state, double* o, int B, int H, int d, int dv, void* stream);
+LA2_API int la2_decode_tokens_f64(const double* q, const double* k, const double* v, const double* decay,
+                                  double* state, double* o, int B, int H, int T, int d, int dv,
+                                  void* stream);
 LA2_API int la2_check_decay_f64(const double* decay, int H, void* stream);
 
 /*

@@ -8,7 +8,9 @@ Public API
   lightning_attn2, LightningAttn2Fn     torch entry point + autograd
   la2_forward, la2_backward             raw passes with state in/out
   chunk_state, chunk_dstate, state_scan sequence-parallel building blocks
-  decode_step                           recurrent decode (tila.inference_step)
+  decode_step, decode_tokens            recurrent decode, one or T tokens per launch
+                                        (tila.inference_step folded over tokens)
+  recurrent_forward                     the per-token recurrence (tila.recurrent_forward)
   sp_lightning_attn2                    sequence parallel over torch.distributed
   tila_api                              the reference's numpy operator API on the GPU
   matrix                                seeded inputs and text fixtures (tila.matrix)
@@ -20,11 +22,13 @@ from .ops import (
     chunk_state,
     decay_tensor,
     decode_step,
+    decode_tokens,
     la2_backward,
     la2_backward_states,
     la2_forward,
     la2_forward_states,
     lightning_attn2,
+    recurrent_forward,
     set_tuning,
     split_backward,
     split_factor,
@@ -42,12 +46,14 @@ __all__ = [
     "chunk_state",
     "decay_tensor",
     "decode_step",
+    "decode_tokens",
     "exclusive_scan",
     "la2_backward",
     "la2_backward_states",
     "la2_forward",
     "la2_forward_states",
     "lightning_attn2",
+    "recurrent_forward",
     "set_tuning",
     "sp_lightning_attn2",
     "split_backward",

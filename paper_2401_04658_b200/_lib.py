@@ -45,6 +45,7 @@ SIGNATURES: dict[str, list] = {
     "la2_chunk_dstate": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_state_scan": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int), _i, _vp],
     "la2_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "la2_decode_tokens": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_check_decay": [_vp, _i, _vp],
     "la2_state_blocks_bytes": [_i, _i, _i, _i, _i],
     "la2_forward_states": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
@@ -53,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "la2_forward_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_backward_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "la2_decode_step_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
+    "la2_decode_tokens_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "la2_check_decay_f64": [_vp, _i, _vp],
     "la2_forward_norm": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_float, _i, _i, _i, _i, _i, _i,
                          _i, _vp],

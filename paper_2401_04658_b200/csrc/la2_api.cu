@@ -696,13 +696,19 @@ int la2_backward_f64(const double* q, const double* k, const double* v, const do
   return launch_f64(k, q, dout, dv, decay, dkv_in, 0, dkv_out, B, H, N, d, dvd, 1, block, st);
 }
 
-int la2_decode_step_f64(const double* q, const double* k, const double* v, const double* decay,
-                        double* state, double* o, int B, int H, int d, int dv, void* stream) {
+int la2_decode_tokens_f64(const double* q, const double* k, const double* v, const double* decay,
+                          double* state, double* o, int B, int H, int T, int d, int dv, void* stream) {
   g_err[0] = 0;
-  if (B < 1 || H < 1 || d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad decode shape");
+  if (B < 1 || H < 1 || d < 1 || dv < 1 || T < 0) return set_error(LA2_ERR_VALUE, "bad decode shape");
+  if (T == 0) return 0;
   if (!q || !k || !v || !decay || !state || !o) return set_error(LA2_ERR_VALUE, "null pointer");
   if (int rc = bind_device(stream, state)) return rc;
-  return launch_decode_f64(q, k, v, decay, state, o, B, H, d, dv, static_cast<cudaStream_t>(stream));
+  return launch_decode_f64(q, k, v, decay, state, o, B, H, d, dv, T, static_cast<cudaStream_t>(stream));
+}
+
+int la2_decode_step_f64(const double* q, const double* k, const double* v, const double* decay,
+                        double* state, double* o, int B, int H, int d, int dv, void* stream) {
+  return la2_decode_tokens_f64(q, k, v, decay, state, o, B, H, 1, d, dv, stream);
 }
 
 int la2_check_decay_f64(const double* decay, int H, void* stream) {
@@ -737,16 +743,22 @@ int la2_check_decay_f64(const double* decay, int H, void* stream) {
   return 0;
 }
 
-int la2_decode_step(const void* q, const void* k, const void* v, const float* decay, float* state,
-                    void* o, int B, int H, int d, int dv, int dtype, void* stream) {
+int la2_decode_tokens(const void* q, const void* k, const void* v, const float* decay, float* state,
+                      void* o, int B, int H, int T, int d, int dv, int dtype, void* stream) {
   g_err[0] = 0;
-  if (B < 1 || H < 1 || d < 1 || dv < 1) return set_error(LA2_ERR_VALUE, "bad decode shape");
+  if (B < 1 || H < 1 || d < 1 || dv < 1 || T < 0) return set_error(LA2_ERR_VALUE, "bad decode shape");
   if (dtype != LA2_BF16 && dtype != LA2_FP32)
     return set_error(LA2_ERR_UNSUPPORTED, "dtype must be LA2_BF16 or LA2_FP32");
+  if (T == 0) return 0;
   if (!q || !k || !v || !decay || !state || !o) return set_error(LA2_ERR_VALUE, "null pointer");
   if (int rc = bind_device(stream, state)) return rc;
-  return launch_decode(q, k, v, decay, state, o, B, H, d, dv, dtype,
+  return launch_decode(q, k, v, decay, state, o, B, H, d, dv, T, dtype,
                        static_cast<cudaStream_t>(stream));
+}
+
+int la2_decode_step(const void* q, const void* k, const void* v, const float* decay, float* state,
+                    void* o, int B, int H, int d, int dv, int dtype, void* stream) {
+  return la2_decode_tokens(q, k, v, decay, state, o, B, H, 1, d, dv, dtype, stream);
 }
 
 }  // extern "C"

@@ -155,12 +155,16 @@ int launch_f64(const double* q, const double* k, const double* v, double* o, con
   return 0;
 }
 
-// One CTA per (b, h); thread (g, j) owns value column j of rows g, g+RG, ...:
+// One CTA per (b, h); thread (g, j) owns value column j of rows g, g+RG, ... ntok tokens
+// per call (q, k: [B*H][ntok][d]; v, o: [B*H][ntok][dv]), each one single step's arithmetic:
 //   new_kv = lam * kv + outer(k, v);  o = q @ new_kv        (_decay_step, reference.py:135-139)
+// so a call over ntok tokens equals ntok one-token calls bit for bit (tila.recurrent_forward
+// continued from the state, reference.py:142-159).
 __global__ void __launch_bounds__(256)
     la2_decode_f64_kernel(const double* __restrict__ q, const double* __restrict__ k,
                           const double* __restrict__ v, const double* __restrict__ decay,
-                          double* __restrict__ state, double* __restrict__ o, int H, int d, int dv) {
+                          double* __restrict__ state, double* __restrict__ o, int H, int d, int dv,
+                          int ntok) {
   extern __shared__ double dsm64[];
   double* qs = dsm64;
   double* ks = qs + d;
@@ -168,41 +172,45 @@ __global__ void __launch_bounds__(256)
   double* red = vs + dv;  // [256]
   const int bh = blockIdx.x;
   const double lam = checked_decay64(decay[bh % H]);
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    qs[e] = q[static_cast<size_t>(bh) * d + e];
-    ks[e] = k[static_cast<size_t>(bh) * d + e];
-  }
-  for (int e = threadIdx.x; e < dv; e += blockDim.x) vs[e] = v[static_cast<size_t>(bh) * dv + e];
-  __syncthreads();
   const int RG = blockDim.x / dv;
   const int g = threadIdx.x / dv, j = threadIdx.x % dv;
-  double acc = 0.0;
-  if (g < RG) {
-    double* Sst = state + static_cast<size_t>(bh) * d * dv;
-    const double vj = vs[j];
-    for (int i = g; i < d; i += RG) {
-      // lam * kv, then += outer(k, v): two roundings, as _decay_step does them
-      const double x = __dadd_rn(__dmul_rn(lam, Sst[static_cast<size_t>(i) * dv + j]), __dmul_rn(ks[i], vj));
-      Sst[static_cast<size_t>(i) * dv + j] = x;
-      acc = fma(qs[i], x, acc);
+  double* Sst = state + static_cast<size_t>(bh) * d * dv;
+  for (int t = 0; t < ntok; ++t) {
+    const size_t row = static_cast<size_t>(bh) * ntok + t;
+    if (t) __syncthreads();  // the previous token's reduction has read red / vs
+    for (int e = threadIdx.x; e < d; e += blockDim.x) {
+      qs[e] = q[row * d + e];
+      ks[e] = k[row * d + e];
     }
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < dv) {
-    double s = 0.0;
-    for (int gg = 0; gg < RG; ++gg) s += red[gg * dv + threadIdx.x];
-    o[static_cast<size_t>(bh) * dv + threadIdx.x] = s;
+    for (int e = threadIdx.x; e < dv; e += blockDim.x) vs[e] = v[row * dv + e];
+    __syncthreads();
+    double acc = 0.0;
+    if (g < RG) {
+      const double vj = vs[j];
+      for (int i = g; i < d; i += RG) {
+        // lam * kv, then += outer(k, v): two roundings, as _decay_step does them
+        const double x = __dadd_rn(__dmul_rn(lam, Sst[static_cast<size_t>(i) * dv + j]), __dmul_rn(ks[i], vj));
+        Sst[static_cast<size_t>(i) * dv + j] = x;
+        acc = fma(qs[i], x, acc);
+      }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < dv) {
+      double s = 0.0;
+      for (int gg = 0; gg < RG; ++gg) s += red[gg * dv + threadIdx.x];
+      o[row * dv + threadIdx.x] = s;
+    }
   }
 }
 
 int launch_decode_f64(const double* q, const double* k, const double* v, const double* decay,
-                      double* state, double* o, int B, int H, int d, int dv, cudaStream_t st) {
+                      double* state, double* o, int B, int H, int d, int dv, int ntok, cudaStream_t st) {
   if (dv > 256 || d > 256) return set_error(LA2_ERR_UNSUPPORTED, "fp64 decode supports d, dv <= 256");
   const size_t smem = sizeof(double) * (2 * d + dv + 256);
   const int threads = (256 / dv) * dv;
   LaunchScope log_scope(st, "la2_decode_f64_kernel", B * H, 1);
-  la2_decode_f64_kernel<<<B * H, threads, smem, st>>>(q, k, v, decay, state, o, H, d, dv);
+  la2_decode_f64_kernel<<<B * H, threads, smem, st>>>(q, k, v, decay, state, o, H, d, dv, ntok);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_decode_f64_kernel launch", e);
   return 0;

@@ -92,12 +92,12 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, int cols, int N, int BH, int
                    long long row_pitch = 0, int box_cols = 64);
 int launch_simt(const FArgs& a, cudaStream_t st);
 // fp64 F pass (la2_f64.cu): one launch of the block recurrence (reverse = F_rev) and
-// the fp64 decode step
+// the fp64 decode (ntok tokens per call)
 int launch_f64(const double* q, const double* k, const double* v, double* o, const double* decay,
                const double* kv_in, int kv_in_T, double* kv_out, int B, int H, int N, int dk, int dv,
                int reverse, int block, cudaStream_t st);
 int launch_decode_f64(const double* q, const double* k, const double* v, const double* decay,
-                      double* state, double* o, int B, int H, int d, int dv, cudaStream_t st);
+                      double* state, double* o, int B, int H, int d, int dv, int ntok, cudaStream_t st);
 // Norm(.) of NormAttention (la2_norm.cu): rows of [B,H,N,dv] normalised per head
 // (group = 1) or over all heads of a token (group = H); rstd [B*H/group*N]
 int launch_rmsnorm_fwd(const void* x, void* y, float* rstd, int B, int H, int N, int dv, int group, float eps,
@@ -105,7 +105,7 @@ int launch_rmsnorm_fwd(const void* x, void* y, float* rstd, int B, int H, int N,
 int launch_rmsnorm_bwd(const void* dy, const void* y, const float* rstd, void* dx, int B, int H, int N, int dv,
                        int group, int dtype, cudaStream_t st);
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
-                  void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st);
+                  void* o, int B, int H, int d, int dv, int ntok, int dtype, cudaStream_t st);
 int launch_state_scan(const float* chunk_states, const float* decay, const float* init,
                       float* prefix, int G, int BH, int H, int dk, int dv, const int* lens,
                       int reverse, cudaStream_t st);

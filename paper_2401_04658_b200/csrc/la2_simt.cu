@@ -182,14 +182,20 @@ int launch_simt(const FArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------- decode
-// One CTA per (b, h); thread (g, j) owns value column j of rows g, g+RG, ...
-// Operation order follows _decay_step (pkg/src/tila/reference.py:135-139):
+// ntok successive decode steps per (b, h): tila.inference_step folded over ntok tokens
+// (pkg/src/tila/reference.py:162-181), i.e. tila.recurrent_forward (:142-159) continued
+// from the given state. Every token runs the arithmetic of a single step in the same
+// order, so one call over ntok tokens equals ntok single-token calls bit for bit.
+// Operation order follows _decay_step (reference.py:135-139):
 //   new_kv = lam * kv + outer(k, v);  o = q @ new_kv
+// q, k: [B*H][ntok][d]; v, o: [B*H][ntok][dv]; state: [B*H][d][dv] fp32, in place.
+//
+// General shapes: one CTA per (b, h); thread (g, j) owns value column j of rows g, g+RG, ...
 template <typename T>
 __global__ void __launch_bounds__(256)
     la2_decode_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                       const float* __restrict__ decay, float* __restrict__ state,
-                      T* __restrict__ o, int H, int d, int dv) {
+                      T* __restrict__ o, int H, int d, int dv, int ntok) {
   extern __shared__ float dsm[];
   float* qs = dsm;
   float* ks = qs + d;
@@ -198,119 +204,221 @@ __global__ void __launch_bounds__(256)
   const int bh = blockIdx.x;
   const int h = bh % H;
   const float lam = checked_decay(decay[h]);
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    qs[e] = ld_el<T>(q + static_cast<size_t>(bh) * d + e);
-    ks[e] = ld_el<T>(k + static_cast<size_t>(bh) * d + e);
-  }
-  for (int e = threadIdx.x; e < dv; e += blockDim.x) vs[e] = ld_el<T>(v + static_cast<size_t>(bh) * dv + e);
-  __syncthreads();
   const int RG = blockDim.x / dv;  // dv <= 256 guaranteed by the launcher
   const int g = threadIdx.x / dv, j = threadIdx.x % dv;
-  float acc = 0.f;
-  if (g < RG) {
-    float* S = state + static_cast<size_t>(bh) * d * dv;
-    const float vj = vs[j];
-    for (int i = g; i < d; i += RG) {
-      const float x = fmaf(lam, S[static_cast<size_t>(i) * dv + j], ks[i] * vj);
-      S[static_cast<size_t>(i) * dv + j] = x;
-      acc = fmaf(qs[i], x, acc);
+  float* S = state + static_cast<size_t>(bh) * d * dv;
+  for (int t = 0; t < ntok; ++t) {
+    const size_t row = static_cast<size_t>(bh) * ntok + t;
+    if (t) __syncthreads();  // the previous token's reduction has read red / vs
+    for (int e = threadIdx.x; e < d; e += blockDim.x) {
+      qs[e] = ld_el<T>(q + row * d + e);
+      ks[e] = ld_el<T>(k + row * d + e);
     }
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < dv) {
-    float s = 0.f;
-    for (int gg = 0; gg < RG; ++gg) s += red[gg * dv + threadIdx.x];
-    st_el<T>(o + static_cast<size_t>(bh) * dv + threadIdx.x, s);
+    for (int e = threadIdx.x; e < dv; e += blockDim.x) vs[e] = ld_el<T>(v + row * dv + e);
+    __syncthreads();
+    float acc = 0.f;
+    if (g < RG) {
+      const float vj = vs[j];
+      for (int i = g; i < d; i += RG) {
+        const float x = fmaf(lam, S[static_cast<size_t>(i) * dv + j], ks[i] * vj);
+        S[static_cast<size_t>(i) * dv + j] = x;
+        acc = fmaf(qs[i], x, acc);
+      }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < dv) {
+      float s = 0.f;
+      for (int gg = 0; gg < RG; ++gg) s += red[gg * dv + threadIdx.x];
+      st_el<T>(o + row * dv + threadIdx.x, s);
+    }
   }
 }
 
-// Bandwidth-shaped decode for d * dv a multiple of 1024 and dv / 4 dividing 256: each of
-// the 256 threads owns PER float4 of the fp32 state (fixed 4 value columns, rows strided
-// by 256 / (dv / 4)), issues all its state loads before any arithmetic (PER x 16 bytes
-// in flight per thread), writes the updated state back and reduces o over rows in smem.
-template <typename T, int PER>
-__global__ void __launch_bounds__(256)
+// 4 consecutive elements <-> float4 (one 8-byte bf16 / 16-byte fp32 access; conversions
+// as ld_el / st_el, so the values are the same bits as element-wise accesses)
+template <typename T> struct Quad;
+template <> struct Quad<float> {
+  using raw = float4;
+  __device__ static float4 f4(raw r) { return r; }
+  __device__ static void st(float* p, float4 x) { *reinterpret_cast<float4*>(p) = x; }
+};
+template <> struct Quad<__nv_bfloat16> {
+  using raw = uint2;
+  __device__ static float4 f4(raw r) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  __device__ static void st(__nv_bfloat16* p, float4 x) {
+    uint2 r;
+    *reinterpret_cast<__nv_bfloat162*>(&r.x) = __floats2bfloat162_rn(x.x, x.y);
+    *reinterpret_cast<__nv_bfloat162*>(&r.y) = __floats2bfloat162_rn(x.z, x.w);
+    *reinterpret_cast<uint2*>(p) = r;
+  }
+};
+
+// Bandwidth-shaped decode: the state's value columns are cut into gridDim.y slices of dvc
+// columns (dvc / 4 dividing 256, d * dvc a multiple of 1024, PER = d * dvc / 1024 <= 8);
+// each of the 256 threads of a CTA owns PER float4 of its slice (fixed 4 value columns,
+// rows strided by 256 / (dvc / 4)), issues all its state loads before any arithmetic and
+// keeps them in registers across the call's tokens: the state crosses HBM once per call,
+// not once per token. Tokens go in chunks of TC: the chunk's q and k rows (one contiguous
+// span each) arrive as 16-byte loads and are staged in smem as fp32, each thread's 4
+// values of v per token as one 8/16-byte load; the next chunk's loads are issued before
+// the current chunk's arithmetic. o is reduced over rows in smem per token. The slicing
+// depends only on (d, dv), so the reduction order -- and every bit of the result -- is
+// the same whatever the number of tokens per call.
+template <typename T, int PER, int TC>
+__global__ void __launch_bounds__(256, TC == 1 ? 3 : 2)
     la2_decode_vec_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                           const float* __restrict__ decay, float* __restrict__ state,
-                          T* __restrict__ o, int H, int d, int dv) {
-  __shared__ float qs[256], ks[256];
-  __shared__ float4 red[256];
+                          T* __restrict__ o, int H, int d, int dv, int dvc, int ntok) {
+  constexpr int EPC = 16 / sizeof(T);                  // elements per 16-byte chunk
+  constexpr int W = (TC * 256 / EPC + 255) / 256;      // 16-byte q (and k) chunks per thread
+  using Raw = typename Quad<T>::raw;
+  __shared__ float qs[TC][256], ks[TC][256];
+  __shared__ float4 red[TC][256];
   const int bh = blockIdx.x, t = threadIdx.x;
+  const int cb = blockIdx.y * dvc;  // first value column of this CTA's slice
   const float lam = checked_decay(decay[bh % H]);
-  if (t < d) {
-    qs[t] = ld_el<T>(q + static_cast<size_t>(bh) * d + t);
-    ks[t] = ld_el<T>(k + static_cast<size_t>(bh) * d + t);
-  }
-  const int C4 = dv >> 2, R = 256 / C4;
+  const int C4 = dvc >> 2, R = 256 / C4, DV4 = dv >> 2;
   const int c4 = t % C4, r0 = t / C4;
-  float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv);
+  float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv + cb);
   float4 x[PER];
 #pragma unroll
-  for (int m = 0; m < PER; ++m) x[m] = S[(r0 + m * R) * C4 + c4];
-  float4 vv;
-  vv.x = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4);
-  vv.y = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 1);
-  vv.z = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 2);
-  vv.w = ld_el<T>(v + static_cast<size_t>(bh) * dv + 4 * c4 + 3);
-  __syncthreads();
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int m = 0; m < PER; ++m) x[m] = S[(r0 + m * R) * DV4 + c4];
+  const size_t row0 = static_cast<size_t>(bh) * ntok;
+  uint4 qa[W], ka[W];
+  Raw vr[TC];
+  auto issue = [&](int c0) {  // global -> registers for the chunk starting at token c0
+    const int tc = min(TC, ntok - c0);
+    const int n16 = tc * d / EPC;
+    const uint4* qsrc = reinterpret_cast<const uint4*>(q + (row0 + c0) * d);
+    const uint4* ksrc = reinterpret_cast<const uint4*>(k + (row0 + c0) * d);
 #pragma unroll
-  for (int m = 0; m < PER; ++m) {
-    const int i = r0 + m * R;
-    const float ki = ks[i], qi = qs[i];
-    float4 y;
-    y.x = fmaf(lam, x[m].x, ki * vv.x);
-    y.y = fmaf(lam, x[m].y, ki * vv.y);
-    y.z = fmaf(lam, x[m].z, ki * vv.z);
-    y.w = fmaf(lam, x[m].w, ki * vv.w);
-    S[i * C4 + c4] = y;
-    acc.x = fmaf(qi, y.x, acc.x);
-    acc.y = fmaf(qi, y.y, acc.y);
-    acc.z = fmaf(qi, y.z, acc.z);
-    acc.w = fmaf(qi, y.w, acc.w);
-  }
-  red[t] = acc;
-  __syncthreads();
-  if (t < C4) {
-    float4 s = red[t];
-    for (int r = 1; r < R; ++r) {
-      const float4 w = red[r * C4 + t];
-      s.x += w.x; s.y += w.y; s.z += w.z; s.w += w.w;
+    for (int w = 0; w < W; ++w) {
+      const int j = t + 256 * w;
+      if (j < n16) {
+        qa[w] = __ldg(qsrc + j);
+        ka[w] = __ldg(ksrc + j);
+      }
     }
-    T* op = o + static_cast<size_t>(bh) * dv + 4 * t;
-    st_el<T>(op, s.x);
-    st_el<T>(op + 1, s.y);
-    st_el<T>(op + 2, s.z);
-    st_el<T>(op + 3, s.w);
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+      if (u < tc) vr[u] = __ldg(reinterpret_cast<const Raw*>(v + (row0 + c0 + u) * dv + cb + 4 * c4));
+  };
+  issue(0);
+  for (int c0 = 0; c0 < ntok; c0 += TC) {
+    const int tc = min(TC, ntok - c0);
+    if (c0) __syncthreads();  // the previous chunk's reduction has read red / qs / ks
+    {  // registers -> smem (fp32)
+      const int n16 = tc * d / EPC;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int j = t + 256 * w;
+        if (j < n16) {
+          const int e0 = j * EPC, u = e0 / d, i = e0 % d;
+          const T* qe = reinterpret_cast<const T*>(&qa[w]);
+          const T* ke = reinterpret_cast<const T*>(&ka[w]);
+#pragma unroll
+          for (int z = 0; z < EPC; ++z) {
+            qs[u][i + z] = static_cast<float>(qe[z]);
+            ks[u][i + z] = static_cast<float>(ke[z]);
+          }
+        }
+      }
+    }
+    float4 vv[TC];
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+      if (u < tc) vv[u] = Quad<T>::f4(vr[u]);
+    if (c0 + TC < ntok) issue(c0 + TC);  // the next chunk's loads overlap this chunk
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < TC; ++u) {
+      if (u < tc) {
+        // packed fp32x2 (FFMA2 / FMUL2): each lane is the scalar step's rounding,
+        // y = fma(lam, x, k * v), acc = fma(q, y, acc)
+        float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+        const float2 l2 = make_float2(lam, lam);
+        const float2 v01 = make_float2(vv[u].x, vv[u].y), v23 = make_float2(vv[u].z, vv[u].w);
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+          const int i = r0 + m * R;
+          const float2 k2 = make_float2(ks[u][i], ks[u][i]), q2 = make_float2(qs[u][i], qs[u][i]);
+          const float2 y01 = __ffma2_rn(l2, make_float2(x[m].x, x[m].y), __fmul2_rn(k2, v01));
+          const float2 y23 = __ffma2_rn(l2, make_float2(x[m].z, x[m].w), __fmul2_rn(k2, v23));
+          x[m] = make_float4(y01.x, y01.y, y23.x, y23.y);
+          a01 = __ffma2_rn(q2, y01, a01);
+          a23 = __ffma2_rn(q2, y23, a23);
+        }
+        red[u][t] = make_float4(a01.x, a01.y, a23.x, a23.y);
+      }
+    }
+    __syncthreads();
+    for (int e = t; e < tc * C4; e += 256) {
+      const int u = e / C4, c = e % C4;
+      float4 s = red[u][c];
+      for (int r = 1; r < R; ++r) {
+        const float4 w = red[u][r * C4 + c];
+        s.x += w.x; s.y += w.y; s.z += w.z; s.w += w.w;
+      }
+      Quad<T>::st(o + (row0 + c0 + u) * dv + cb + 4 * c, s);
+    }
   }
+#pragma unroll
+  for (int m = 0; m < PER; ++m) S[(r0 + m * R) * DV4 + c4] = x[m];
+}
+
+// Column slice of the vector decode for (d, dv), or 0 when the shape does not fit it:
+// the widest slice with at most 8 float4 of state per thread.
+static int decode_vec_slice(int d, int dv) {
+  if (d > 256 || dv % 4) return 0;
+  for (int dvc = dv; dvc >= 4; dvc >>= 1) {
+    if (dv % dvc || dvc % 4 || 256 % (dvc / 4) || (d * dvc) % 1024) break;
+    if (d * dvc / 1024 <= 8) return dvc;
+    if (dvc % 8) break;
+  }
+  return 0;
 }
 
 template <typename T>
 static bool launch_decode_vec(const void* q, const void* k, const void* v, const float* decay,
-                              float* state, void* o, int B, int H, int d, int dv, cudaStream_t st) {
-  if (dv % 4 || 256 % (dv / 4) || (d * dv) % 1024 || d > 256) return false;
-  const int per = d * dv / 1024;
+                              float* state, void* o, int B, int H, int d, int dv, int ntok, cudaStream_t st) {
+  const int dvc = decode_vec_slice(d, dv);
+  // 16-byte q / k chunks within a row, 4-element v / o accesses aligned
+  const uintptr_t al = reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k);
+  const uintptr_t al4 = reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o);
+  if (dvc == 0 || (d * sizeof(T)) % 16 || al % 16 || al4 % (4 * sizeof(T))) return false;
+  const int per = d * dvc / 1024;
+  const dim3 grid(B * H, dv / dvc);
   const T* tq = static_cast<const T*>(q);
   const T* tk = static_cast<const T*>(k);
   const T* tv = static_cast<const T*>(v);
   T* to = static_cast<T*>(o);
+  // one token: a 1-token chunk (6 KB of smem, more CTAs per SM for the HBM-bound step)
   switch (per) {
-#define LA2_DEC(P) \
-  case P: la2_decode_vec_kernel<T, P><<<B * H, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv); return true;
-    LA2_DEC(1) LA2_DEC(2) LA2_DEC(4) LA2_DEC(8) LA2_DEC(16) LA2_DEC(32)
+#define LA2_DEC(P)                                                                                       \
+  case P:                                                                                                \
+    if (ntok == 1)                                                                                       \
+      la2_decode_vec_kernel<T, P, 1><<<grid, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok); \
+    else                                                                                                 \
+      la2_decode_vec_kernel<T, P, 8><<<grid, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok); \
+    return true;
+    LA2_DEC(1) LA2_DEC(2) LA2_DEC(4) LA2_DEC(8)
 #undef LA2_DEC
     default: return false;
   }
 }
 
 int launch_decode(const void* q, const void* k, const void* v, const float* decay, float* state,
-                  void* o, int B, int H, int d, int dv, int dtype, cudaStream_t st) {
+                  void* o, int B, int H, int d, int dv, int ntok, int dtype, cudaStream_t st) {
   if (dv > 256) return set_error(LA2_ERR_UNSUPPORTED, "decode supports dv <= 256");
   LaunchScope log_scope(st, "la2_decode_kernel", B * H, 1);
   const bool vec = (dtype == LA2_FP32)
-                       ? launch_decode_vec<float>(q, k, v, decay, state, o, B, H, d, dv, st)
-                       : launch_decode_vec<__nv_bfloat16>(q, k, v, decay, state, o, B, H, d, dv, st);
+                       ? launch_decode_vec<float>(q, k, v, decay, state, o, B, H, d, dv, ntok, st)
+                       : launch_decode_vec<__nv_bfloat16>(q, k, v, decay, state, o, B, H, d, dv, ntok, st);
   if (vec) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("la2_decode_vec_kernel launch", e);
@@ -321,12 +429,12 @@ int launch_decode(const void* q, const void* k, const void* v, const float* deca
   if (dtype == LA2_FP32)
     la2_decode_kernel<float><<<B * H, threads, smem, st>>>(
         static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v),
-        decay, state, static_cast<float*>(o), H, d, dv);
+        decay, state, static_cast<float*>(o), H, d, dv, ntok);
   else
     la2_decode_kernel<__nv_bfloat16><<<B * H, threads, smem, st>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
         static_cast<const __nv_bfloat16*>(v), decay, state, static_cast<__nv_bfloat16*>(o), H, d,
-        dv);
+        dv, ntok);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("la2_decode_kernel launch", e);
   return 0;

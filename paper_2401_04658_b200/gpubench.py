@@ -22,7 +22,8 @@ reference applies to its own CPU kernel:
 
 Implementations (``impl``): "tiled" = la2_forward / la2_backward on [1,1,n,d]
 tensors (the reference's single-head shape), "chunked" = STREAM_CHUNKS calls with
-the carried fp32 state, "recurrent" = one la2_decode_step per token. The
+the carried fp32 state, "recurrent" = the per-token recurrence in one launch
+(ops.recurrent_forward: la2_decode_tokens, the state held on chip). The
 reference's "oracle" (O(n^2) CPU) has no GPU counterpart here.
 
 * ``acceptance_scaling``                 -- pkg/tests/test_acceptance.py:51-62, :129-144
@@ -131,9 +132,7 @@ def _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads=1, bat
                     _, state = ops.la2_forward(q[:, :, a:b], k[:, :, a:b], v[:, :, a:b], dec,
                                                kv_in=state, output_final_state=True)
         else:
-            st = torch.zeros(batch, heads, d, dv, device=device)
-            for t in range(n):
-                ops.decode_step(q[:, :, t], k[:, :, t], v[:, :, t], dec, st)
+            ops.recurrent_forward(q, k, v, dec)
 
     def backward():
         ops.la2_backward(q, k, v, do, dec)
@@ -145,8 +144,8 @@ def _make_pass(impl, direction, n, d, dv, lam, dtype, seed, device, heads=1, bat
         outputs = {"forward": o_b, "backward": g_b, "fwd+bwd": max(o_b, g_b)}[direction]
     elif impl == "chunked":  # a chunk's o and the carried state, each old and new
         outputs = 2 * batch * heads * -(-n // STREAM_CHUNKS) * dv * e + 2 * st_b
-    else:  # the state and one step's o (old and new)
-        outputs = st_b + 2 * batch * heads * dv * e
+    else:  # o and the state
+        outputs = o_b + st_b
 
     if direction == "forward":
         return forward, outputs

@@ -581,6 +581,52 @@ def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.T
     return o
 
 
+def decode_tokens(q, k, v, decay: DecayLike, state: torch.Tensor) -> torch.Tensor:
+    """T recurrent decode steps in one launch, in place on ``state`` (fp32 ``[B,H,d,dv]``;
+    float64 for float64 inputs): :func:`decode_step` folded over the T tokens -- the
+    same arithmetic per token, so bit-identical to T single steps -- with the state held
+    on chip across the tokens (multi-token decode: a speculative draft, a short chunk of
+    a stream). q, k: ``[B,H,T,d]``; v: ``[B,H,T,dv]``; returns o ``[B,H,T,dv]``
+    (tila.inference_step folded over rows, reference.py:162-181 -- tila.recurrent_forward
+    continued from the state, reference.py:142-159).
+    """
+    if q.dim() != 4 or k.shape != q.shape or v.dim() != 4 or v.shape[:3] != q.shape[:3]:
+        raise ValueError("decode_tokens expects q, k [B,H,T,d] and v [B,H,T,dv]")
+    B, H, T, d = q.shape
+    dv = v.shape[3]
+    sdt = _F64 if q.dtype == _F64 else torch.float32
+    if tuple(state.shape) != (B, H, d, dv) or state.dtype != sdt or not state.is_contiguous():
+        raise ValueError(f"state must be a contiguous {sdt} tensor of shape {(B, H, d, dv)}")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ValueError("q, k, v must share a dtype")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(v)
+    if q.dtype == _F64:
+        dec = _decay(decay, H, q.device, _F64)
+        _lib.call("la2_decode_tokens_f64", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(state), _ptr(o),
+                  B, H, T, d, dv, _stream(q.device))
+        return o
+    dec = _decay(decay, H, q.device)
+    _lib.call("la2_decode_tokens", _ptr(q), _ptr(k), _ptr(v), _ptr(dec), _ptr(state), _ptr(o),
+              B, H, T, d, dv, _code(q), _stream(q.device))
+    return o
+
+
+def recurrent_forward(q, k, v, decay: DecayLike, initial_state: Optional[torch.Tensor] = None):
+    """Per-token recurrent forward (tila.recurrent_forward, reference.py:142-159): the
+    O(N d dv) recurrence token by token from a zero (or the given) state. Returns
+    ``(o, final_state)``. The tiled kernels are the throughput path; this is the
+    recurrence itself, kept on the GPU for cross-checks and short streams.
+    """
+    B, H, N, d, dv = _check_qkv(q, k, v)
+    sdt = _F64 if q.dtype == _F64 else torch.float32
+    if initial_state is None:
+        st = torch.zeros(B, H, d, dv, device=q.device, dtype=sdt)
+    else:
+        st = _state(initial_state, B, H, d, dv, q.device, "initial_state", sdt).clone()
+    return decode_tokens(q, k, v, decay, st), st
+
+
 # ------------------------------------------------------------------- autograd
 # d = dv = 64 bf16 training: the forward stores its per-block states and the backward runs
 # dQ / dK / dV as one 3-CTA cluster (la2_forward_states / la2_backward_states); False: the

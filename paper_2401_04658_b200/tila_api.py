@@ -2,8 +2,10 @@
 
 Same names, argument meaning and error behaviour as the reference ``tila``
 package (pkg/src/tila/__init__.py:13-40), so the reference's own test suite runs
-against this module (tests/test_gpu_reference_suites.py: 220 of its 222 tests pass;
-the other two assert bitwise equality with NumPy/OpenBLAS summation orders):
+against this module (tests/test_gpu_reference_suites.py: 221 of its 222 tests pass; the
+other asserts bitwise equality between inference_step and the reference's own
+recurrent_forward, i.e. NumPy/OpenBLAS summation order -- it passes when
+recurrent_forward is served from here too):
 
   tiled_forward(q, k, v, lam, block)            pkg/src/tila/kernel.py:122-139
   chunked_forward(q, k, v, lam, block, state)   pkg/src/tila/kernel.py:142-162
@@ -11,6 +13,7 @@ the other two assert bitwise equality with NumPy/OpenBLAS summation orders):
   batched_forward(inputs, block, parallel)      pkg/src/tila/kernel.py:252-260
   batched_backward(inputs, block, parallel)     pkg/src/tila/kernel.py:263-266
   inference_step(q_t, k_t, v_t, state, lam)     pkg/src/tila/reference.py:162-181
+  recurrent_forward(q, k, v, lam)               pkg/src/tila/reference.py:142-159
   random_matrix, save_fixture, load_fixture,    pkg/src/tila/matrix.py (re-exported from
   AttentionConfig, FixtureFormatError           ``matrix``: seeded inputs, text fixtures)
 
@@ -237,3 +240,21 @@ def inference_step(q_t, k_t, v_t, state: KvState, lam: float):
     o = ops.decode_step(_dev(q_t, dev, dt).reshape(1, 1, d), _dev(k_t, dev, dt).reshape(1, 1, d),
                         _dev(v_t, dev, dt).reshape(1, 1, dv), [float(lam)], st)
     return _host(o.reshape(dv), dt), KvState(_host(st.reshape(d, dv), dt), state.tokens_absorbed + 1)
+
+
+def recurrent_forward(q, k, v, lam: float):
+    """Per-token recurrent forward (reference.py:142-159) on the GPU decode kernels: one
+    launch folds all n tokens through the recurrence (la2_decode_tokens[_f64]), each with
+    inference_step's arithmetic, so folding :func:`inference_step` over the rows
+    reproduces it bit for bit, as the reference's docstring promises."""
+    q, k, v = _check_inputs(q, k, v)
+    _check_decay(lam)
+    n, d = q.shape
+    dv = v.shape[1]
+    dt = q.dtype
+    if n == 0 or d == 0 or dv == 0:  # nothing to launch; the reference's values
+        return np.zeros((n, dv), dt), KvState(np.zeros((d, dv), dt), n)
+    dev = _device()
+    o, st = ops.recurrent_forward(_dev(q, dev, dt)[None, None], _dev(k, dev, dt)[None, None],
+                                  _dev(v, dev, dt)[None, None], [float(lam)])
+    return _host(o[0, 0], dt), KvState(_host(st[0, 0], dt), n)

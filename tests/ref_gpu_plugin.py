@@ -8,8 +8,14 @@ chunked_forward, batched_forward, batched_backward, inference_step
 (paper_2401_04658_b200.tila_api), in the ``tila`` namespace the tests import from and in
 ``tila.verify`` (which imports them by name). Everything else (oracles, recurrence, power
 tables, fixtures, CLI, bench) stays the reference's own code, so every kernel-level
-assertion of the suite compares the GPU against the reference. TEST INFRASTRUCTURE ONLY.
+assertion of the suite compares the GPU against the reference. With
+LA2_REF_PATCH_RECURRENT=1 the per-token recurrence (tila.recurrent_forward) is served by
+the GPU too (la2_decode_tokens), so the reference's recurrence tests (test_reference.py)
+check the GPU recurrence against its oracle, hand values and the inference_step fold.
+TEST INFRASTRUCTURE ONLY.
 """
+
+import os
 
 import sys
 from pathlib import Path
@@ -21,6 +27,8 @@ for p in (ROOT / "oracle" / "_ref", ROOT):
 
 PATCHED = ("tiled_forward", "tiled_backward", "chunked_forward", "batched_forward", "batched_backward",
            "inference_step")
+if os.environ.get("LA2_REF_PATCH_RECURRENT") == "1":
+    PATCHED = PATCHED + ("recurrent_forward",)
 
 
 def pytest_configure(config):

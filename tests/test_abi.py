@@ -146,6 +146,18 @@ def test_f64_entry_points_validate_without_device(lib):
                                 1, 1, 8, 4, 4, 0, None) == _lib.LA2_ERR_VALUE
     assert lib.la2_decode_step_f64(dummy, dummy, dummy, dummy, None, dummy, 1, 1, 4, 4,
                                    None) == _lib.LA2_ERR_VALUE
+    # multi-token decode: T < 0 rejected, T = 0 a no-op before any device work
+    assert lib.la2_decode_tokens_f64(dummy, dummy, dummy, dummy, dummy, dummy, 1, 1, -1, 4, 4,
+                                     None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_decode_tokens_f64(dummy, dummy, dummy, dummy, dummy, dummy, 1, 1, 0, 4, 4, None) == 0
+    assert lib.la2_decode_tokens(dummy, dummy, dummy, dummy, dummy, dummy, 1, 1, -1, 4, 4, _lib.LA2_FP32,
+                                 None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_decode_tokens(dummy, dummy, dummy, dummy, dummy, dummy, 1, 1, 0, 4, 4, _lib.LA2_FP32,
+                                 None) == 0
+    assert lib.la2_decode_tokens(dummy, dummy, dummy, dummy, None, dummy, 1, 1, 3, 4, 4, _lib.LA2_FP32,
+                                 None) == _lib.LA2_ERR_VALUE
+    assert lib.la2_decode_tokens(dummy, dummy, dummy, dummy, dummy, dummy, 1, 1, 3, 4, 4, 7,
+                                 None) == _lib.LA2_ERR_UNSUPPORTED
     good = (ctypes.c_double * 3)(0.5, 1.0, 1e-300)
     assert lib.la2_check_decay_f64(good, 3, None) == 0
     for vals in ((0.5, 1.0000000001), (0.5, 0.0), (0.5, float("nan"))):

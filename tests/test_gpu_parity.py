@@ -357,6 +357,99 @@ def test_prefill_decode_multitoken_stream():
     assert rel(torch.cat(outs, 2), po) <= BF16_TOL and rel(st, pkv) <= BF16_TOL
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
+@pytest.mark.parametrize("d,dv", [(64, 64), (128, 128), (128, 256), (64, 32), (12, 20), (256, 8)])
+def test_decode_tokens_equals_single_steps_bitwise(dtype, d, dv):
+    """la2_decode_tokens over T tokens == T la2_decode_step calls, bit for bit (state and
+    every output row), for the register-resident vector kernel (d*dv a multiple of 1024),
+    the general kernel (12 x 20, 256 x 8) and fp64; T spans partial and several 8-token
+    chunks. Also against the fp64 recurrence of the oracle port."""
+    B, H = 2, 3
+    decay = [0.5, 0.999, 1.0]
+    for T in (1, 5, 19):
+        q, k, v, _ = inputs(B, H, T, d, dv, dtype, seed=T + d)
+        init = rand((B, H, d, dv), 99, torch.float64 if dtype == torch.float64 else torch.float32)
+        qg, kg, vg = gpu(q, k, v)
+        st1 = init.to(DEV).clone()
+        rows = [la2.decode_step(qg[:, :, t], kg[:, :, t], vg[:, :, t], decay, st1) for t in range(T)]
+        stT = init.to(DEV).clone()
+        oT = la2.decode_tokens(qg, kg, vg, decay, stT)
+        assert torch.equal(oT, torch.stack(rows, 2)), (T, dtype, d, dv)
+        assert torch.equal(stT, st1), (T, dtype, d, dv)
+        # against the fp64 recurrence from the same state (tila.recurrent_forward continued)
+        S = init.double().numpy().copy()
+        ref = np.zeros((B, H, T, dv))
+        Q, K, V = to64(q), to64(k), to64(v)
+        for b in range(B):
+            for h in range(H):
+                for t in range(T):
+                    S[b, h] = decay[h] * S[b, h] + np.outer(K[b, h, t], V[b, h, t])
+                    ref[b, h, t] = Q[b, h, t] @ S[b, h]
+        tol = 1e-12 if dtype == torch.float64 else (BF16_TOL if dtype == torch.bfloat16 else FP32_TOL)
+        assert rel(oT, ref) <= tol and rel(stT, S) <= max(tol, 1e-6)
+
+
+def test_recurrent_forward_against_reference_golden(golden):
+    """GPU per-token recurrence (one la2_decode_tokens_f64 launch) vs the reference's own
+    tila.recurrent_forward outputs on its grid (golden.npz, fp64) and the tiled final
+    state; and the inference_step fold reproduces it bit for bit (reference.py:142-148)."""
+    def proj(a, tag):  # the fixture's projection (tests/test_oracle.py)
+        a = np.asarray(a, np.float64)
+        w = np.random.default_rng([7919, tag, a.shape[0], a.shape[1]]).standard_normal((16, a.size))
+        return w @ a.ravel()
+
+    def err(got, ci, name):
+        ref = golden[f"grid/{ci}/{name}/proj"]
+        e = np.max(np.abs(proj(got, ci) - ref)) / max(np.max(np.abs(ref)), 1e-12)
+        full = f"grid/{ci}/{name}/full"
+        if full in golden:
+            e = max(e, port.rel_err(got, golden[full]))
+        return e
+
+    worst = 0.0
+    for ci, m in enumerate(golden["grid/meta"]):
+        n, d, dv, lam, seed = int(m[0]), int(m[1]), int(m[2]), float(m[4]), int(m[5])
+        q, k, v, _ = port.case_inputs(n, d, dv, seed)
+        o, st = tila_api.recurrent_forward(q, k, v, lam)
+        worst = max(worst, err(o, ci, "recurrent_o"), err(st.kv, ci, "tiled_kv"))
+        assert st.tokens_absorbed == n
+    print("recurrent_forward vs reference, worst rel err:", worst)
+    assert worst <= 1e-11
+    q, k, v, _ = port.case_inputs(32, 6, 9, 33)
+    full, final = tila_api.recurrent_forward(q, k, v, 0.9)
+    state = tila_api.KvState.fresh(6, 9)
+    rows = []
+    for t in range(32):
+        o, state = tila_api.inference_step(q[t], k[t], v[t], state, 0.9)
+        rows.append(o)
+    assert np.array_equal(np.stack(rows), full) and np.array_equal(state.kv, final.kv)
+    # the reference's edge values: n = 0, lam = 1 cumulative sum, input validation
+    o, st = tila_api.recurrent_forward(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 2)), 0.5)
+    assert o.shape == (0, 2) and st.kv.shape == (3, 2) and st.tokens_absorbed == 0
+    o, _ = tila_api.recurrent_forward(np.ones((4, 1)), np.ones((4, 1)), np.ones((4, 1)), 1.0)
+    assert o.ravel().tolist() == [1.0, 2.0, 3.0, 4.0]
+    with pytest.raises(ValueError):
+        tila_api.recurrent_forward(np.ones((2, 2)), np.ones((2, 2)), np.ones((2, 2)), 1.5)
+
+
+def test_decode_tokens_continues_a_prefill():
+    """Serving: prefill with the tensor-core forward, then a multi-token decode (a 7-token
+    draft) from its final state, then single steps -- equal to the one-shot forward."""
+    B, H, D = 2, 4, 128
+    N0, T1, T2 = 1000, 7, 3
+    N = N0 + T1 + T2
+    decay = [0.9, 0.99, 0.999, 1.0]
+    q, k, v, _ = inputs(B, H, N, D, D, torch.bfloat16, seed=5)
+    qg, kg, vg = gpu(q, k, v)
+    o0, st = la2.la2_forward(qg[:, :, :N0].contiguous(), kg[:, :, :N0].contiguous(), vg[:, :, :N0].contiguous(),
+                             decay, output_final_state=True)
+    o1 = la2.decode_tokens(qg[:, :, N0:N0 + T1], kg[:, :, N0:N0 + T1], vg[:, :, N0:N0 + T1], decay, st)
+    o2 = [la2.decode_step(qg[:, :, t], kg[:, :, t], vg[:, :, t], decay, st).unsqueeze(2)
+          for t in range(N0 + T1, N)]
+    po, pkv = port.bhnd_forward(to64(q), to64(k), to64(v), decay)
+    assert rel(torch.cat([o0, o1, *o2], 2), po) <= BF16_TOL and rel(st, pkv) <= BF16_TOL
+
+
 # ------------------------------------------------------------- tila mirror API
 def test_tila_api_kats():
     ones = [[1.0], [1.0]]
@@ -635,9 +728,9 @@ def test_gpubench_sweep_and_block_invariance():
     """GPU harness: a doubling sweep yields one record per (impl, n) and a verdict;
     block sizes never change results (bench.py:264-292)."""
     from paper_2401_04658_b200 import gpubench as gb
-    recs, verdicts = gb.scaling_sweep(["tiled", "chunked"], [256, 512, 1024, 2048], 64,
+    recs, verdicts = gb.scaling_sweep(["tiled", "chunked", "recurrent"], [256, 512, 1024, 2048], 64,
                                       reps=3, heads=4)
-    assert len(recs) == 8 and [v.impl for v in verdicts] == ["tiled", "chunked"]
+    assert len(recs) == 12 and [v.impl for v in verdicts] == ["tiled", "chunked", "recurrent"]
     assert all(r.median_seconds > 0 and not r.oom for r in recs)
     assert all(len(v.ratios) == 3 for v in verdicts)
     rows = gb.block_size_sweep(512, 64, 0.9, [16, 64, 256], reps=3)

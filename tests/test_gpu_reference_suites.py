@@ -54,6 +54,8 @@ def gpu_verify(tila, monkeypatch):
     monkeypatch.setattr(v, "tiled_forward", tila_api.tiled_forward)
     monkeypatch.setattr(v, "tiled_backward", tila_api.tiled_backward)
     monkeypatch.setattr(v, "chunked_forward", tila_api.chunked_forward)
+    # "recurrent vs oracle" then checks the GPU recurrence (la2_decode_tokens) too
+    monkeypatch.setattr(v, "recurrent_forward", tila_api.recurrent_forward)
     return v
 
 
@@ -116,6 +118,7 @@ def test_patch_is_effective(gpu_verify, tila):
     assert gpu_verify.tiled_forward is tila_api.tiled_forward
     assert gpu_verify.tiled_backward is tila_api.tiled_backward
     assert gpu_verify.chunked_forward is tila_api.chunked_forward
+    assert gpu_verify.recurrent_forward is tila_api.recurrent_forward
     assert tila.tiled_forward is not tila_api.tiled_forward
 
 
@@ -127,25 +130,45 @@ EXPECTED_BITWISE = {
 }
 
 
-def test_reference_test_suite_against_gpu(tila):
-    """The reference's OWN test suite (pkg/tests, staged to oracle/_ref/tests) with tila's
-    kernel entry points served by the GPU adapter (tests/ref_gpu_plugin.py): every test
-    passes except the ones asserting bitwise equality with NumPy's summation order."""
+def _run_reference_tests(targets, extra_env=None):
     import os
     import re
     import subprocess
 
-    tests = REF / "tests"
-    if not (tests / "test_kernel.py").exists():
-        pytest.skip("reference test suite not staged (oracle/build_ref.py)")
-    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(ROOT / "tests"), str(REF), str(ROOT)]))
-    cmd = [sys.executable, "-m", "pytest", str(tests), "-p", "ref_gpu_plugin", "-q", "-rf", "-c", os.devnull,
-           "--rootdir", str(REF), "-p", "no:cacheprovider"]
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(ROOT / "tests"), str(REF), str(ROOT)]),
+               **(extra_env or {}))
+    cmd = [sys.executable, "-m", "pytest", *map(str, targets), "-p", "ref_gpu_plugin", "-q", "-rf", "-c",
+           os.devnull, "--rootdir", str(REF), "-p", "no:cacheprovider"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
     out = res.stdout + res.stderr
     failed = {m.split("tests/", 1)[-1] for m in re.findall(r"FAILED (\S+)", out)}
     summary = re.findall(r"(\d+) passed", out)
-    passed = int(summary[-1]) if summary else 0
+    return (int(summary[-1]) if summary else 0), failed, out
+
+
+def test_reference_recurrence_tests_with_gpu_recurrence(tila):
+    """The reference's recurrence tests (pkg/tests/test_reference.py) with
+    recurrent_forward ALSO served by the GPU (one la2_decode_tokens launch): its oracle
+    cross-checks (1e-12 / 1e-11), hand values, the lam=1 cumulative sum, and the
+    bitwise inference_step fold -- which passes here, because the multi-token decode
+    runs each token with the single step's arithmetic."""
+    tests = REF / "tests"
+    if not (tests / "test_reference.py").exists():
+        pytest.skip("reference test suite not staged (oracle/build_ref.py)")
+    passed, failed, out = _run_reference_tests([tests / "test_reference.py"],
+                                               {"LA2_REF_PATCH_RECURRENT": "1"})
+    print(f"reference recurrence tests on the GPU recurrence: {passed} passed, failed: {sorted(failed)}")
+    assert passed >= 20 and not failed, out[-3000:]
+
+
+def test_reference_test_suite_against_gpu(tila):
+    """The reference's OWN test suite (pkg/tests, staged to oracle/_ref/tests) with tila's
+    kernel entry points served by the GPU adapter (tests/ref_gpu_plugin.py): every test
+    passes except the ones asserting bitwise equality with NumPy's summation order."""
+    tests = REF / "tests"
+    if not (tests / "test_kernel.py").exists():
+        pytest.skip("reference test suite not staged (oracle/build_ref.py)")
+    passed, failed, out = _run_reference_tests([tests])
     print(f"reference suite on the GPU adapter: {passed} passed, failed: {sorted(failed)}")
     assert passed >= 200, out[-3000:]
     assert failed <= EXPECTED_BITWISE, out[-3000:]
