@@ -239,13 +239,12 @@ __global__ void __launch_bounds__(256)
 // as ld_el / st_el, so the values are the same bits as element-wise accesses)
 template <typename T> struct Quad;
 template <> struct Quad<float> {
-  using raw = float4;
-  __device__ static float4 f4(raw r) { return r; }
+  __device__ static float4 ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
   __device__ static void st(float* p, float4 x) { *reinterpret_cast<float4*>(p) = x; }
 };
 template <> struct Quad<__nv_bfloat16> {
-  using raw = uint2;
-  __device__ static float4 f4(raw r) {
+  __device__ static float4 ld(const __nv_bfloat16* p) {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
     const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
     const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
     return make_float4(a.x, a.y, b.x, b.y);
@@ -258,155 +257,171 @@ template <> struct Quad<__nv_bfloat16> {
   }
 };
 
-// Bandwidth-shaped decode: the state's value columns are cut into gridDim.y slices of dvc
-// columns (dvc / 4 dividing 256, d * dvc a multiple of 1024, PER = d * dvc / 1024 <= 8);
-// each of the 256 threads of a CTA owns PER float4 of its slice (fixed 4 value columns,
-// rows strided by 256 / (dvc / 4)), issues all its state loads before any arithmetic and
-// keeps them in registers across the call's tokens: the state crosses HBM once per call,
-// not once per token. Tokens go in chunks of TC: the chunk's q and k rows (one contiguous
-// span each) arrive as 16-byte loads and are staged in smem as fp32, each thread's 4
-// values of v per token as one 8/16-byte load; the next chunk's loads are issued before
-// the current chunk's arithmetic. o is reduced over rows in smem per token. The slicing
-// depends only on (d, dv), so the reduction order -- and every bit of the result -- is
-// the same whatever the number of tokens per call.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Bandwidth-shaped decode. Thread layout: a CTA covers dvc value columns of one head
+// (gridDim.y = dv / dvc slices) with (dvc / 4) x R threads; thread (r0, c4) owns the
+// float4 of columns [4 c4, 4 c4 + 4) in rows r0, r0 + R, ..., r0 + (PER - 1) R
+// (R = d / PER). It loads them once, runs the call's tokens on them in registers and
+// writes them back once: the state crosses HBM once per call, not once per token. o is
+// reduced over rows in smem per token (the thread's PER-row fma chain, then the R row
+// groups in order). (PER, R) depend only on (d, dv) -- the slice width only changes how
+// many CTAs share a head -- so every bit of the result is the same whatever the number
+// of tokens per call: T tokens in one call == T one-token calls.
+// Tokens go in chunks of TC: the chunk's q, k rows (one contiguous span each) and v
+// slices arrive by cp.async into smem, double-buffered (the next chunk's copies are in
+// flight during the current chunk's packed-fp32x2 arithmetic).
 template <typename T, int PER, int TC>
-__global__ void __launch_bounds__(256, TC == 1 ? 3 : 2)
+__global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
     la2_decode_vec_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                           const float* __restrict__ decay, float* __restrict__ state,
                           T* __restrict__ o, int H, int d, int dv, int dvc, int ntok) {
-  constexpr int EPC = 16 / sizeof(T);                  // elements per 16-byte chunk
-  constexpr int W = (TC * 256 / EPC + 255) / 256;      // 16-byte q (and k) chunks per thread
-  using Raw = typename Quad<T>::raw;
-  __shared__ float qs[TC][256], ks[TC][256];
-  __shared__ float4 red[TC][256];
-  const int bh = blockIdx.x, t = threadIdx.x;
+  constexpr int NB = TC == 1 ? 1 : 2;         // staging buffers
+  constexpr int EPC = 16 / sizeof(T);         // elements per 16-byte copy (q, k)
+  constexpr int EP8 = 8 / sizeof(T);          // elements per 8-byte copy (v)
+  extern __shared__ __align__(16) unsigned char dsm_dec[];
+  const int nt = blockDim.x, t = threadIdx.x, bh = blockIdx.x;
+  float4* red = reinterpret_cast<float4*>(dsm_dec);  // [TC][nt]
+  T* qr = reinterpret_cast<T*>(red + TC * nt);       // [NB][TC][d]
+  T* kr = qr + NB * TC * d;                          // [NB][TC][d]
+  T* vr = kr + NB * TC * d;                          // [NB][TC][dvc]
   const int cb = blockIdx.y * dvc;  // first value column of this CTA's slice
   const float lam = checked_decay(decay[bh % H]);
-  const int C4 = dvc >> 2, R = 256 / C4, DV4 = dv >> 2;
+  const int C4 = dvc >> 2, R = d / PER, DV4 = dv >> 2;
   const int c4 = t % C4, r0 = t / C4;
   float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv + cb);
   float4 x[PER];
 #pragma unroll
   for (int m = 0; m < PER; ++m) x[m] = S[(r0 + m * R) * DV4 + c4];
   const size_t row0 = static_cast<size_t>(bh) * ntok;
-  uint4 qa[W], ka[W];
-  Raw vr[TC];
-  auto issue = [&](int c0) {  // global -> registers for the chunk starting at token c0
+  auto issue = [&](int c0, int buf) {  // chunk at token c0 -> staging buffer buf
     const int tc = min(TC, ntok - c0);
     const int n16 = tc * d / EPC;
-    const uint4* qsrc = reinterpret_cast<const uint4*>(q + (row0 + c0) * d);
-    const uint4* ksrc = reinterpret_cast<const uint4*>(k + (row0 + c0) * d);
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const int j = t + 256 * w;
-      if (j < n16) {
-        qa[w] = __ldg(qsrc + j);
-        ka[w] = __ldg(ksrc + j);
-      }
+    const T* qs = q + (row0 + c0) * d;
+    const T* ks = k + (row0 + c0) * d;
+    T* qd = qr + buf * TC * d;
+    T* kd = kr + buf * TC * d;
+    for (int j = t; j < n16; j += nt) {
+      cp_async16(qd + j * EPC, qs + j * EPC);
+      cp_async16(kd + j * EPC, ks + j * EPC);
     }
-#pragma unroll
-    for (int u = 0; u < TC; ++u)
-      if (u < tc) vr[u] = __ldg(reinterpret_cast<const Raw*>(v + (row0 + c0 + u) * dv + cb + 4 * c4));
+    const int per_row = dvc / EP8, n8 = tc * per_row;
+    T* vd = vr + buf * TC * dvc;
+    for (int j = t; j < n8; j += nt) {
+      const int u = j / per_row, w = j % per_row;
+      cp_async8(vd + u * dvc + w * EP8, v + (row0 + c0 + u) * dv + cb + w * EP8);
+    }
+    cp_async_commit();
   };
-  issue(0);
-  for (int c0 = 0; c0 < ntok; c0 += TC) {
+  issue(0, 0);
+  // TC == 1 is launched for single tokens only: one trip, the state stored as computed
+  for (int c0 = 0, it = 0; TC == 1 ? it < 1 : c0 < ntok; c0 += TC, ++it) {
     const int tc = min(TC, ntok - c0);
-    if (c0) __syncthreads();  // the previous chunk's reduction has read red / qs / ks
-    {  // registers -> smem (fp32)
-      const int n16 = tc * d / EPC;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const int j = t + 256 * w;
-        if (j < n16) {
-          const int e0 = j * EPC, u = e0 / d, i = e0 % d;
-          const T* qe = reinterpret_cast<const T*>(&qa[w]);
-          const T* ke = reinterpret_cast<const T*>(&ka[w]);
-#pragma unroll
-          for (int z = 0; z < EPC; ++z) {
-            qs[u][i + z] = static_cast<float>(qe[z]);
-            ks[u][i + z] = static_cast<float>(ke[z]);
-          }
-        }
-      }
+    const int buf = (NB == 2) ? (it & 1) : 0;
+    if (it) __syncthreads();  // chunk it-1 is done with red and its staging buffer
+    if (NB == 2 && c0 + TC < ntok) {
+      issue(c0 + TC, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    float4 vv[TC];
-#pragma unroll
-    for (int u = 0; u < TC; ++u)
-      if (u < tc) vv[u] = Quad<T>::f4(vr[u]);
-    if (c0 + TC < ntok) issue(c0 + TC);  // the next chunk's loads overlap this chunk
     __syncthreads();
+    const T* qb = qr + buf * TC * d;
+    const T* kb = kr + buf * TC * d;
+    const T* vb = vr + buf * TC * dvc;
 #pragma unroll
     for (int u = 0; u < TC; ++u) {
       if (u < tc) {
         // packed fp32x2 (FFMA2 / FMUL2): each lane is the scalar step's rounding,
         // y = fma(lam, x, k * v), acc = fma(q, y, acc)
+        const float4 vv = Quad<T>::ld(vb + u * dvc + 4 * c4);
         float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
         const float2 l2 = make_float2(lam, lam);
-        const float2 v01 = make_float2(vv[u].x, vv[u].y), v23 = make_float2(vv[u].z, vv[u].w);
+        const float2 v01 = make_float2(vv.x, vv.y), v23 = make_float2(vv.z, vv.w);
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
           const int i = r0 + m * R;
-          const float2 k2 = make_float2(ks[u][i], ks[u][i]), q2 = make_float2(qs[u][i], qs[u][i]);
+          const float kf = static_cast<float>(kb[u * d + i]), qf = static_cast<float>(qb[u * d + i]);
+          const float2 k2 = make_float2(kf, kf), q2 = make_float2(qf, qf);
           const float2 y01 = __ffma2_rn(l2, make_float2(x[m].x, x[m].y), __fmul2_rn(k2, v01));
           const float2 y23 = __ffma2_rn(l2, make_float2(x[m].z, x[m].w), __fmul2_rn(k2, v23));
           x[m] = make_float4(y01.x, y01.y, y23.x, y23.y);
+          if (TC == 1) S[i * DV4 + c4] = x[m];
           a01 = __ffma2_rn(q2, y01, a01);
           a23 = __ffma2_rn(q2, y23, a23);
         }
-        red[u][t] = make_float4(a01.x, a01.y, a23.x, a23.y);
+        red[u * nt + t] = make_float4(a01.x, a01.y, a23.x, a23.y);
       }
     }
     __syncthreads();
-    for (int e = t; e < tc * C4; e += 256) {
+    for (int e = t; e < tc * C4; e += nt) {
       const int u = e / C4, c = e % C4;
-      float4 s = red[u][c];
+      float4 s = red[u * nt + c];
       for (int r = 1; r < R; ++r) {
-        const float4 w = red[u][r * C4 + c];
+        const float4 w = red[u * nt + r * C4 + c];
         s.x += w.x; s.y += w.y; s.z += w.z; s.w += w.w;
       }
       Quad<T>::st(o + (row0 + c0 + u) * dv + cb + 4 * c, s);
     }
   }
+  if (TC != 1) {
 #pragma unroll
-  for (int m = 0; m < PER; ++m) S[(r0 + m * R) * DV4 + c4] = x[m];
+    for (int m = 0; m < PER; ++m) S[(r0 + m * R) * DV4 + c4] = x[m];
+  }
 }
 
-// Column slice of the vector decode for (d, dv), or 0 when the shape does not fit it:
-// the widest slice with at most 8 float4 of state per thread.
-static int decode_vec_slice(int d, int dv) {
+// Row split of the vector decode for (d, dv): PER rows per thread (a power of two <= 16
+// dividing d, ~d*dv/1024), or 0 when the shape does not fit it.
+static int decode_vec_per(int d, int dv) {
   if (d > 256 || dv % 4) return 0;
-  for (int dvc = dv; dvc >= 4; dvc >>= 1) {
-    if (dv % dvc || dvc % 4 || 256 % (dvc / 4) || (d * dvc) % 1024) break;
-    if (d * dvc / 1024 <= 8) return dvc;
-    if (dvc % 8) break;
-  }
-  return 0;
+  int per = 1;
+  while (2 * per <= 16 && 2 * per * 1024 <= d * dv && d % (2 * per) == 0) per *= 2;
+  return per;
 }
 
 template <typename T>
 static bool launch_decode_vec(const void* q, const void* k, const void* v, const float* decay,
                               float* state, void* o, int B, int H, int d, int dv, int ntok, cudaStream_t st) {
-  const int dvc = decode_vec_slice(d, dv);
-  // 16-byte q / k chunks within a row, 4-element v / o accesses aligned
+  const int per = decode_vec_per(d, dv);
+  // 16-byte q / k copies within a row; 8-byte v copies and 4-element o stores aligned
   const uintptr_t al = reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k);
   const uintptr_t al4 = reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o);
-  if (dvc == 0 || (d * sizeof(T)) % 16 || al % 16 || al4 % (4 * sizeof(T))) return false;
-  const int per = d * dvc / 1024;
+  if (per == 0 || (d * sizeof(T)) % 16 || al % 16 || al4 % (4 * sizeof(T))) return false;
+  // value-column slice: the widest with at most 256 threads (one token) / 128 threads
+  // (several: more, smaller CTAs to overlap the per-chunk barriers)
+  const int R = d / per, cap = (ntok == 1) ? 256 : 128;
+  int dvc = dv;
+  while ((dvc / 4) * R > cap && dvc % 8 == 0) dvc /= 2;
+  if ((dvc / 4) * R > cap) return false;
+  const int nt = (dvc / 4) * R;
   const dim3 grid(B * H, dv / dvc);
+  const int tc = (ntok == 1) ? 1 : 8, nb = (ntok == 1) ? 1 : 2;
+  const size_t smem = static_cast<size_t>(tc) * nt * 16 + static_cast<size_t>(nb) * tc * (2 * d + dvc) * sizeof(T);
   const T* tq = static_cast<const T*>(q);
   const T* tk = static_cast<const T*>(k);
   const T* tv = static_cast<const T*>(v);
   T* to = static_cast<T*>(o);
-  // one token: a 1-token chunk (6 KB of smem, more CTAs per SM for the HBM-bound step)
-  switch (per) {
-#define LA2_DEC(P)                                                                                       \
-  case P:                                                                                                \
-    if (ntok == 1)                                                                                       \
-      la2_decode_vec_kernel<T, P, 1><<<grid, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok); \
-    else                                                                                                 \
-      la2_decode_vec_kernel<T, P, 8><<<grid, 256, 0, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok); \
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, nt, smem, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok);
     return true;
-    LA2_DEC(1) LA2_DEC(2) LA2_DEC(4) LA2_DEC(8)
+  };
+  switch (per) {
+#define LA2_DEC(P) \
+  case P: return ntok == 1 ? go(la2_decode_vec_kernel<T, P, 1>) : go(la2_decode_vec_kernel<T, P, 8>);
+    LA2_DEC(1) LA2_DEC(2) LA2_DEC(4) LA2_DEC(8) LA2_DEC(16)
 #undef LA2_DEC
     default: return false;
   }

@@ -31,6 +31,11 @@ pytestmark = pytest.mark.gpu
     # the fused Norm(.) epilogue (the two row warps of a quarter exchange row sums in smem)
     ("racecheck", "1,3,700,64,n"),
     ("memcheck", "2,40,700,64,n"),
+    # multi-token decode (register-resident state slices, chunked q/k staging, next-chunk
+    # prefetch): a partial last chunk, two column slices per head at d = 128
+    ("memcheck", "2,3,19,128,t"),
+    ("racecheck", "2,3,19,128,t"),
+    ("initcheck", "1,2,11,64,t"),
 ])
 def test_sanitizer_clean(tool, shape):
     if not os.path.exists(SAN):
