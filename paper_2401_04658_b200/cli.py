@@ -109,11 +109,10 @@ def run_equivalence(grid: str, seeds, tol_override=None) -> list:
                         outs.append(oc)
                 reports.append(Report(f"chunked {tag}", rel_err(torch.cat(outs, 2), ref), tol))
                 reports.append(Report(f"chunked final state {tag}", rel_err(state, kv), tol))
-                if n <= 256:  # recurrent decode, one token per launch (reference.py:162-181)
-                    st = torch.zeros(1, len(lams), d, dv, device=dev)
-                    rec = torch.stack([ops.decode_step(q[:, :, t], k[:, :, t], v[:, :, t], lam, st)
-                                       for t in range(n)], 2)
-                    reports.append(Report(f"recurrent {tag}", rel_err(rec, ref), tol))
+                # the per-token recurrence, all n tokens in one launch (reference.py:142-159)
+                rec, rst = ops.recurrent_forward(q, k, v, lam)
+                reports.append(Report(f"recurrent {tag}", rel_err(rec, ref), tol))
+                reports.append(Report(f"recurrent final state {tag}", rel_err(rst, kv), tol))
                 grads = ops.la2_backward(q, k, v, do, lam)[:3]
                 for name, g, rg in zip(("dq", "dk", "dv"), grads, _ref_grads(q, k, v, do, lam)):
                     reports.append(Report(f"backward {name} {tag}", rel_err(g, rg), tol))
@@ -244,7 +243,9 @@ def _cmd_stream_demo(args) -> int:
     print(f"streamed {chunks} chunks of {chunk} tokens (d={d}, lambda={lam}, {str(dtype).split('.')[-1]}); "
           f"tokens absorbed: {total}")
     print(f"final state checksum: {float(state.double().sum()):.12e}")
-    one_shot, ref_state = ops.la2_forward(q, k, v, lam_t, output_final_state=True)
+    # one-shot recompute by the per-token recurrence, as the reference's demo does
+    # (pkg/src/tila/cli.py:179: recurrent_forward)
+    one_shot, ref_state = ops.recurrent_forward(q, k, v, lam_t)
     tol = TOL[dtype]
     e_o, e_s = rel_err(streamed, one_shot), rel_err(state, ref_state)
     ok = e_o <= tol and e_s <= tol
