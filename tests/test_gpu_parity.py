@@ -675,6 +675,49 @@ def test_autograd_backward_on_fresh_thread():
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_host_threads_on_separate_streams_bitwise():
+    """Four host threads, each on its own stream, run forward + backward (the replay path
+    with its forked dQ stream, and the stored-state triple) and multi-token decode on
+    different inputs at once; every result equals the same call made alone, bit for bit
+    (the fork / join events and the per-stream workspaces are not shared across threads)."""
+    import threading
+    D, H, N = 64, 4, 2048
+    decay = la2.decay_tensor([0.9, 0.99, 0.999, 1.0], H, torch.device(DEV))
+
+    def job(seed):
+        q, k, v, do = gpu(*inputs(1, H, N, D, D, torch.bfloat16, seed=seed))
+        o, _ = la2.la2_forward(q, k, v, decay)
+        g = la2.la2_backward(q, k, v, do, decay)
+        _, _, blocks = la2.ops.la2_forward_states(q, k, v, decay)
+        gs = la2.ops.la2_backward_states(q, k, v, do, decay, blocks)
+        st = torch.zeros(1, H, D, D, device=DEV)
+        od = la2.decode_tokens(q[:, :, :13], k[:, :, :13], v[:, :, :13], decay, st)
+        return [o, *g[:3], *gs[:3], od, st]
+
+    seeds = [11, 12, 13, 14]
+    alone = []
+    for sd in seeds:
+        alone.append(job(sd))
+        torch.cuda.synchronize()
+    results = [None] * len(seeds)
+
+    def worker(i):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for _ in range(3):
+                results[i] = job(seeds[i])
+            torch.cuda.current_stream().synchronize()
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(seeds))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    for i in range(len(seeds)):
+        for j, (x, y) in enumerate(zip(results[i], alone[i])):
+            assert torch.equal(x, y), (i, j)
+
+
 def test_concurrent_backward_and_graph_capture():
     """The dQ scan on a forked side stream gives bitwise the same gradients as the serial
     order, and the fork/join is capturable in a CUDA graph (replay == eager)."""
