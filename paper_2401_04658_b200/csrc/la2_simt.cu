@@ -413,8 +413,12 @@ static bool launch_decode_vec(const void* q, const void* k, const void* v, const
   const T* tv = static_cast<const T*>(v);
   T* to = static_cast<T*>(o);
   auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // > 48 KB of dynamic smem (fp32 with d > 128, several tokens) needs the opt-in
+    if (smem > 48 * 1024) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return false;
+    }
     kern<<<grid, nt, smem, st>>>(tq, tk, tv, decay, state, to, H, d, dv, dvc, ntok);
     return true;
   };

@@ -358,7 +358,7 @@ def test_prefill_decode_multitoken_stream():
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
-@pytest.mark.parametrize("d,dv", [(64, 64), (128, 128), (128, 256), (64, 32), (12, 20), (256, 8)])
+@pytest.mark.parametrize("d,dv", [(64, 64), (128, 128), (128, 256), (256, 256), (64, 32), (12, 20), (256, 8)])
 def test_decode_tokens_equals_single_steps_bitwise(dtype, d, dv):
     """la2_decode_tokens over T tokens == T la2_decode_step calls, bit for bit (state and
     every output row), for the register-resident vector kernel (d*dv a multiple of 1024),
