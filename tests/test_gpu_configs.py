@@ -6,6 +6,9 @@
   C4  B=4  H=20 N=16384 d=128   80 pair units > 74 co-resident clusters
   C5  B=1  H=16 N=524288 d=128  one long sequence on one GPU: intra-GPU 8-way sequence
                                  split (chunk states, state scan, carried passes)
+  C2 x4 B=8 H=16 N=262144 d=64  the headline shape at 4x the sequence: 2^31 elements per
+                                 tensor (4 GiB bf16), so any 32-bit flat index overflows;
+                                 the stored-state training path (forward states + triple)
 
 Each runs the production entry point (``lightning_attn2`` forward + autograd backward)
 on the full configuration and compares a subset of heads with the fp64 oracle port
@@ -120,5 +123,17 @@ def test_c5_one_gpu_parity():
     picks = [(0, 0), (0, 1), (0, 2)]  # lam = 1, 0.99999, 0.9999
     errs = run_config(B, H, N, D, C5_DECAY, picks, seed=2)
     print("C5 rel errors:", errs)
+    worst = max(max(e.values()) for e in errs.values())
+    assert worst <= BF16_TOL, errs
+
+
+def test_c2_at_2g_elements_parity():
+    B, H, N, D = 8, 16, 262144, 64
+    assert B * H * N * D == 2 ** 31
+    # the last head (highest addresses), the first, and the lam = 1 / 0.99999 heads
+    picks = [(7, 15), (0, 0), (0, 6), (7, 5)]
+    errs = run_config(B, H, N, D, C3_DECAY, picks, seed=3)
+    print("C2 x4 rel errors:", errs)
+    assert {1.0, 0.99999} <= {lam for (_, _, lam) in errs}
     worst = max(max(e.values()) for e in errs.values())
     assert worst <= BF16_TOL, errs
