@@ -49,6 +49,14 @@ def _stream(dev: torch.device) -> int:
                                               torch.cuda.current_device())
 
 
+def _on(device: torch.device, **tensors) -> None:
+    """Every named tensor must be a CUDA tensor on ``device``: a host (or other-device)
+    pointer reaching a kernel would fault and poison the CUDA context. There is no CPU path."""
+    for name, t in tensors.items():
+        if t is not None and (not t.is_cuda or t.device != device):
+            raise ValueError(f"{name} must be a CUDA tensor on {device}, got one on {t.device}")
+
+
 def decay_tensor(decay: DecayLike, H: int, device: torch.device, dtype=torch.float32) -> torch.Tensor:
     """Per-head decay as a contiguous float32 [H] tensor on ``device``.
 
@@ -247,6 +255,7 @@ def split_forward(q, k, v, decay, g: int, kv_in=None, output_final_state=False):
 def split_backward(q, k, v, d_out, decay, g: int, prefix, dkv_in=None, output_dkv=False):
     """Backward matching :func:`split_forward` (prefix = its chunk-carried states)."""
     B, H, N, d, dv = _check_qkv(q, k, v)
+    _on(q.device, d_out=d_out)
     dec = _decay(decay, H, q.device)
     dec_g = dec.repeat_interleave(g)
     q4, k4, v4, do4 = (_chunked(t.contiguous(), g) for t in (q, k, v, d_out))
@@ -336,6 +345,7 @@ def la2_backward_states(q, k, v, d_out, decay: DecayLike, kv_blocks: torch.Tenso
         raise ValueError("stored per-block states need bf16 with d = dv = 64")
     if d_out.shape != v.shape or d_out.dtype != v.dtype:
         raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
+    _on(q.device, d_out=d_out, kv_blocks=kv_blocks)
     nblk = (N + 127) // 128
     if (tuple(kv_blocks.shape) != (B, H, nblk, d, dv) or kv_blocks.dtype != torch.bfloat16
             or not kv_blocks.is_contiguous()):
@@ -366,6 +376,7 @@ def rmsnorm_forward(x: torch.Tensor, eps: float = 1e-6, norm: str = "head", out:
     features of a token ("heads"). Returns ``(y, rstd)``; ``out=x`` normalises in place."""
     B, H, N, dv = x.shape
     grp = _norm_group(norm, H)
+    _on(x.device, x=x, out=out)
     x = x.contiguous()
     y = torch.empty_like(x) if out is None else out
     rstd = torch.empty(B, H // grp, N, device=x.device, dtype=torch.float32)
@@ -378,6 +389,7 @@ def rmsnorm_backward(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor, norm
     """dx = (dy - y mean(dy y)) rstd, the backward of :func:`rmsnorm_forward`."""
     B, H, N, dv = y.shape
     grp = _norm_group(norm, H)
+    _on(y.device, y=y, dy=dy, rstd=rstd)
     dy = dy.to(y.dtype).contiguous()
     dx = torch.empty_like(y)
     _lib.call("la2_rmsnorm_backward", _ptr(dy), _ptr(y), _ptr(rstd), _ptr(dx), B, H, N, dv, grp, _code(y),
@@ -440,6 +452,7 @@ def la2_backward(q, k, v, d_out, decay: DecayLike, kv_in=None, dkv_in=None, outp
     B, H, N, d, dv = _check_qkv(q, k, v)
     if d_out.shape != v.shape or d_out.dtype != v.dtype:
         raise ValueError(f"d_out must have shape {tuple(v.shape)} and dtype {v.dtype}")
+    _on(q.device, d_out=d_out)
     if q.dtype == _F64:
         dec = _decay(decay, H, q.device, _F64)
         kv_in = _state(kv_in, B, H, d, dv, q.device, "kv_in", _F64)
@@ -567,6 +580,7 @@ def decode_step(q_t, k_t, v_t, decay: DecayLike, state: torch.Tensor) -> torch.T
         raise ValueError(f"state must be a contiguous {sdt} tensor of shape {(B, H, d, dv)}")
     if not (q_t.dtype == k_t.dtype == v_t.dtype):
         raise ValueError("q_t, k_t, v_t must share a dtype")
+    _on(state.device, state=state, q_t=q_t, k_t=k_t, v_t=v_t)
     q_t, k_t, v_t = q_t.contiguous(), k_t.contiguous(), v_t.contiguous()
     if q_t.dtype == _F64:
         dec = _decay(decay, H, q_t.device, _F64)
@@ -599,6 +613,7 @@ def decode_tokens(q, k, v, decay: DecayLike, state: torch.Tensor) -> torch.Tenso
         raise ValueError(f"state must be a contiguous {sdt} tensor of shape {(B, H, d, dv)}")
     if not (q.dtype == k.dtype == v.dtype):
         raise ValueError("q, k, v must share a dtype")
+    _on(state.device, state=state, q=q, k=k, v=v)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     o = torch.empty_like(v)
     if q.dtype == _F64:

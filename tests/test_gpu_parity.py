@@ -718,6 +718,27 @@ def test_host_threads_on_separate_streams_bitwise():
             assert torch.equal(x, y), (i, j)
 
 
+def test_mixed_device_arguments_refused():
+    """A host tensor among device tensors is refused with ValueError before any launch (a
+    host pointer in a kernel would fault and poison the context); the context stays usable."""
+    q, k, v, do = gpu(*inputs(1, 2, 256, 64, 64, torch.bfloat16, seed=3))
+    st = torch.zeros(1, 2, 64, 64, device=DEV)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.la2_backward(q, k, v, do.cpu(), [0.9, 0.99])
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.decode_step(q[:, :, 0].cpu(), k[:, :, 0], v[:, :, 0], [0.9, 0.99], st)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.decode_tokens(q, k, v, [0.9, 0.99], st.cpu())
+    _, _, blocks = la2.ops.la2_forward_states(q, k, v, [0.9, 0.99])
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.ops.la2_backward_states(q, k, v, do, [0.9, 0.99], blocks.cpu())
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.ops.rmsnorm_backward(do, do, torch.zeros(1, 2, 256))
+    o, _ = la2.la2_forward(q, k, v, [0.9, 0.99])
+    torch.cuda.synchronize()
+    assert torch.isfinite(o.float()).all()
+
+
 def test_concurrent_backward_and_graph_capture():
     """The dQ scan on a forked side stream gives bitwise the same gradients as the serial
     order, and the fork/join is capturable in a CUDA graph (replay == eager)."""

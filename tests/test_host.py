@@ -26,6 +26,19 @@ def test_cpu_tensors_refused():
     q = torch.zeros(1, 2, 8, 64)
     with pytest.raises(ValueError, match="CUDA"):
         la2.lightning_attn2(q, q, q, [0.9, 0.9])
+    # every entry point refuses host tensors before any device work (a host pointer
+    # reaching a kernel would fault): decode, multi-token decode, recurrence, Norm(.)
+    st = torch.zeros(1, 2, 64, 64)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.decode_step(q[:, :, 0], q[:, :, 0], q[:, :, 0], [0.9, 0.9], st)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.decode_tokens(q, q, q, [0.9, 0.9], st)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.recurrent_forward(q, q, q, [0.9, 0.9])
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.ops.rmsnorm_forward(q)
+    with pytest.raises(ValueError, match="CUDA"):
+        la2.ops.rmsnorm_backward(q, q, torch.zeros(1, 2, 8))
 
 
 def test_shape_errors():
