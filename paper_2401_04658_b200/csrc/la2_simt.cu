@@ -8,6 +8,8 @@
 //   * la2_scan_kernel   -- prefix/suffix combine of chunk states (sequence parallel).
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "la2_kernels.h"
 
 namespace la2 {
@@ -272,7 +274,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Bandwidth-shaped decode. Thread layout: a CTA covers dvc value columns of one head
 // (gridDim.y = dv / dvc slices) with (dvc / 4) x R threads; thread (r0, c4) owns the
-// float4 of columns [4 c4, 4 c4 + 4) in rows r0, r0 + R, ..., r0 + (PER - 1) R
+// float4 of columns [4 c4, 4 c4 + 4) in the PER consecutive rows r0 PER ... r0 PER + PER - 1
 // (R = d / PER). It loads them once, runs the call's tokens on them in registers and
 // writes them back once: the state crosses HBM once per call, not once per token. o is
 // reduced over rows in smem per token (the thread's PER-row fma chain, then the R row
@@ -281,7 +283,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // of tokens per call: T tokens in one call == T one-token calls.
 // Tokens go in chunks of TC: the chunk's q, k rows (one contiguous span each) and v
 // slices arrive by cp.async into smem, double-buffered (the next chunk's copies are in
-// flight during the current chunk's packed-fp32x2 arithmetic).
+// flight during the current chunk's packed-fp32x2 arithmetic); bf16 q, k are widened to
+// fp32 once per chunk, so a thread reads its rows' values as float4.
 template <typename T, int PER, int TC>
 __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
     la2_decode_vec_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
@@ -290,20 +293,26 @@ __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
   constexpr int NB = TC == 1 ? 1 : 2;         // staging buffers
   constexpr int EPC = 16 / sizeof(T);         // elements per 16-byte copy (q, k)
   constexpr int EP8 = 8 / sizeof(T);          // elements per 8-byte copy (v)
+  // bf16 rows widened to fp32 in smem once per chunk (several tokens); a single token
+  // reads its rows' bf16 values directly (no extra pass and barrier on the HBM-bound step)
+  constexpr bool WIDEN = !std::is_same<T, float>::value && TC > 1;
   extern __shared__ __align__(16) unsigned char dsm_dec[];
   const int nt = blockDim.x, t = threadIdx.x, bh = blockIdx.x;
-  float4* red = reinterpret_cast<float4*>(dsm_dec);  // [TC][nt]
-  T* qr = reinterpret_cast<T*>(red + TC * nt);       // [NB][TC][d]
-  T* kr = qr + NB * TC * d;                          // [NB][TC][d]
-  T* vr = kr + NB * TC * d;                          // [NB][TC][dvc]
+  float4* red = reinterpret_cast<float4*>(dsm_dec);          // [TC][nt]
+  float* qw = reinterpret_cast<float*>(red + TC * nt);       // [TC][d] fp32 (bf16 inputs)
+  float* kw = qw + (WIDEN ? TC * d : 0);                     // [TC][d]
+  T* qr = reinterpret_cast<T*>(kw + (WIDEN ? TC * d : 0));   // [NB][TC][d] as loaded
+  T* kr = qr + NB * TC * d;                                  // [NB][TC][d]
+  T* vr = kr + NB * TC * d;                                  // [NB][TC][dvc]
   const int cb = blockIdx.y * dvc;  // first value column of this CTA's slice
   const float lam = checked_decay(decay[bh % H]);
   const int C4 = dvc >> 2, R = d / PER, DV4 = dv >> 2;
   const int c4 = t % C4, r0 = t / C4;
-  float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv + cb);
+  float4* S = reinterpret_cast<float4*>(state + static_cast<size_t>(bh) * d * dv + cb) +
+              static_cast<size_t>(r0) * PER * DV4 + c4;  // this thread's first row
   float4 x[PER];
 #pragma unroll
-  for (int m = 0; m < PER; ++m) x[m] = S[(r0 + m * R) * DV4 + c4];
+  for (int m = 0; m < PER; ++m) x[m] = S[m * DV4];
   const size_t row0 = static_cast<size_t>(bh) * ntok;
   auto issue = [&](int c0, int buf) {  // chunk at token c0 -> staging buffer buf
     const int tc = min(TC, ntok - c0);
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
   for (int c0 = 0, it = 0; TC == 1 ? it < 1 : c0 < ntok; c0 += TC, ++it) {
     const int tc = min(TC, ntok - c0);
     const int buf = (NB == 2) ? (it & 1) : 0;
-    if (it) __syncthreads();  // chunk it-1 is done with red and its staging buffer
+    if (it) __syncthreads();  // chunk it-1 is done with red, the fp32 rows and its buffer
     if (NB == 2 && c0 + TC < ntok) {
       issue(c0 + TC, buf ^ 1);
       cp_async_wait<1>();
@@ -337,12 +346,64 @@ __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
       cp_async_wait<0>();
     }
     __syncthreads();
-    const T* qb = qr + buf * TC * d;
-    const T* kb = kr + buf * TC * d;
+    const float* qb = nullptr;
+    const float* kb = nullptr;
+    if constexpr (WIDEN) {  // bf16 -> fp32 once per chunk (exact), 8 elements per step
+      const T* qs = qr + buf * TC * d;
+      const T* ks = kr + buf * TC * d;
+      for (int j = t; j < tc * d / 8; j += nt) {
+        const uint4 a = *reinterpret_cast<const uint4*>(qs + 8 * j);
+        const uint4 b = *reinterpret_cast<const uint4*>(ks + 8 * j);
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+        float2* qd = reinterpret_cast<float2*>(qw + 8 * j);
+        float2* kd = reinterpret_cast<float2*>(kw + 8 * j);
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          qd[z] = __bfloat1622float2(a2[z]);
+          kd[z] = __bfloat1622float2(b2[z]);
+        }
+      }
+      __syncthreads();
+      qb = qw;
+      kb = kw;
+    } else if constexpr (std::is_same<T, float>::value) {
+      qb = reinterpret_cast<const float*>(qr + buf * TC * d);
+      kb = reinterpret_cast<const float*>(kr + buf * TC * d);
+    }
     const T* vb = vr + buf * TC * dvc;
 #pragma unroll
     for (int u = 0; u < TC; ++u) {
       if (u < tc) {
+        // this thread's PER rows of k and q for token u (float4 loads when PER % 4 == 0)
+        float kf[PER], qf[PER];
+        if constexpr (!WIDEN && !std::is_same<T, float>::value) {  // single bf16 token
+          const T* kq = kr + buf * TC * d + u * d + r0 * PER;
+          const T* qq = qr + buf * TC * d + u * d + r0 * PER;
+#pragma unroll
+          for (int m = 0; m < PER; ++m) {
+            kf[m] = static_cast<float>(kq[m]);
+            qf[m] = static_cast<float>(qq[m]);
+          }
+        } else if constexpr (PER % 4 == 0) {
+          const float* kq = kb + u * d + r0 * PER;
+          const float* qq = qb + u * d + r0 * PER;
+#pragma unroll
+          for (int j = 0; j < PER / 4; ++j) {
+            const float4 a = reinterpret_cast<const float4*>(kq)[j];
+            const float4 b = reinterpret_cast<const float4*>(qq)[j];
+            kf[4 * j] = a.x; kf[4 * j + 1] = a.y; kf[4 * j + 2] = a.z; kf[4 * j + 3] = a.w;
+            qf[4 * j] = b.x; qf[4 * j + 1] = b.y; qf[4 * j + 2] = b.z; qf[4 * j + 3] = b.w;
+          }
+        } else {
+          const float* kq = kb + u * d + r0 * PER;
+          const float* qq = qb + u * d + r0 * PER;
+#pragma unroll
+          for (int m = 0; m < PER; ++m) {
+            kf[m] = kq[m];
+            qf[m] = qq[m];
+          }
+        }
         // packed fp32x2 (FFMA2 / FMUL2): each lane is the scalar step's rounding,
         // y = fma(lam, x, k * v), acc = fma(q, y, acc)
         const float4 vv = Quad<T>::ld(vb + u * dvc + 4 * c4);
@@ -351,13 +412,11 @@ __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
         const float2 v01 = make_float2(vv.x, vv.y), v23 = make_float2(vv.z, vv.w);
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
-          const int i = r0 + m * R;
-          const float kf = static_cast<float>(kb[u * d + i]), qf = static_cast<float>(qb[u * d + i]);
-          const float2 k2 = make_float2(kf, kf), q2 = make_float2(qf, qf);
+          const float2 k2 = make_float2(kf[m], kf[m]), q2 = make_float2(qf[m], qf[m]);
           const float2 y01 = __ffma2_rn(l2, make_float2(x[m].x, x[m].y), __fmul2_rn(k2, v01));
           const float2 y23 = __ffma2_rn(l2, make_float2(x[m].z, x[m].w), __fmul2_rn(k2, v23));
           x[m] = make_float4(y01.x, y01.y, y23.x, y23.y);
-          if (TC == 1) S[i * DV4 + c4] = x[m];
+          if (TC == 1) S[m * DV4] = x[m];
           a01 = __ffma2_rn(q2, y01, a01);
           a23 = __ffma2_rn(q2, y23, a23);
         }
@@ -377,7 +436,7 @@ __global__ void __launch_bounds__(TC == 1 ? 256 : 128, TC == 1 ? 2 : 4)
   }
   if (TC != 1) {
 #pragma unroll
-    for (int m = 0; m < PER; ++m) S[(r0 + m * R) * DV4 + c4] = x[m];
+    for (int m = 0; m < PER; ++m) S[m * DV4] = x[m];
   }
 }
 
@@ -407,7 +466,9 @@ static bool launch_decode_vec(const void* q, const void* k, const void* v, const
   const int nt = (dvc / 4) * R;
   const dim3 grid(B * H, dv / dvc);
   const int tc = (ntok == 1) ? 1 : 8, nb = (ntok == 1) ? 1 : 2;
-  const size_t smem = static_cast<size_t>(tc) * nt * 16 + static_cast<size_t>(nb) * tc * (2 * d + dvc) * sizeof(T);
+  const size_t widen = (sizeof(T) == 4 || tc == 1) ? 0 : static_cast<size_t>(2) * tc * d * sizeof(float);
+  const size_t smem = static_cast<size_t>(tc) * nt * 16 + widen +
+                      static_cast<size_t>(nb) * tc * (2 * d + dvc) * sizeof(T);
   const T* tq = static_cast<const T*>(q);
   const T* tk = static_cast<const T*>(k);
   const T* tv = static_cast<const T*>(v);
