@@ -192,8 +192,10 @@ LA2_API int la2_decode_step(const void* q, const void* k, const void* v, const f
  * over T tokens (reference.py:162-181), i.e. tila.recurrent_forward (reference.py:142-159)
  * continued from `state` (a zeroed state gives recurrent_forward itself). Each token
  * runs the single step's arithmetic in the same order, so the result equals T calls of
- * la2_decode_step bit for bit; the state crosses HBM once per call instead of once per
- * token (multi-token decode: speculative / chunked continuation of a stream).
+ * la2_decode_step bit for bit (given the same kernel choice: the vector kernel needs
+ * 16-byte aligned q, k, 4-element aligned v, o and d * sizeof(elem) % 16 == 0, else the
+ * general kernel runs); the state crosses HBM once per call instead of once per token
+ * (multi-token decode: speculative / chunked continuation of a stream).
  * q,k: [B,H,T,d]  v,o: [B,H,T,dv]  state: [B,H,d,dv] fp32. T = 0 is a no-op.
  */
 LA2_API int la2_decode_tokens(const void* q, const void* k, const void* v, const float* decay,
