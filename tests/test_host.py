@@ -200,3 +200,29 @@ def test_cuda_decay_check_cache(monkeypatch):
     ops._check_cuda_decay(w.float(), w)
     ops._check_cuda_decay(w.float(), w)
     assert len(calls) == 4
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference: rank 0 times the reference's own CPU implementation and
+    prints the contract's JSON line (impl, metric, value, cpu_baseline, e2e with zero
+    copy bytes); under torchrun the other ranks exit 0 without work or output."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    base = [sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
+            "--batch", "1", "--heads", "2", "--seq-len", "512", "--cpu-sample-heads", "2"]
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run(base, cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "", (r.stdout, r.stderr[-2000:])
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run(base, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
