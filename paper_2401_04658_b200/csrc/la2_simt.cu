@@ -275,6 +275,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef LA2_DEC1_THREADS
 #define LA2_DEC1_THREADS 128  // CTA size cap of the single-token decode (A/B: tools/ab_decode_cta.sh)
 #endif
+#ifndef LA2_DECT_THREADS
+#define LA2_DECT_THREADS 128  // ... and of the multi-token decode
+#endif
 
 // Bandwidth-shaped decode. Thread layout: a CTA covers dvc value columns of one head
 // (gridDim.y = dv / dvc slices) with (dvc / 4) x R threads; thread (r0, c4) owns the
@@ -290,7 +293,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // flight during the current chunk's packed-fp32x2 arithmetic); bf16 q, k are widened to
 // fp32 once per chunk, so a thread reads its rows' values as float4.
 template <typename T, int PER, int TC>
-__global__ void __launch_bounds__(TC == 1 ? LA2_DEC1_THREADS : 128, TC == 1 ? 512 / LA2_DEC1_THREADS : 4)
+__global__ void __launch_bounds__(TC == 1 ? LA2_DEC1_THREADS : LA2_DECT_THREADS,
+                                  512 / (TC == 1 ? LA2_DEC1_THREADS : LA2_DECT_THREADS))
     la2_decode_vec_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                           const float* __restrict__ decay, float* __restrict__ state,
                           T* __restrict__ o, int H, int d, int dv, int dvc, int ntok) {
@@ -463,7 +467,7 @@ static bool launch_decode_vec(const void* q, const void* k, const void* v, const
   if (per == 0 || (d * sizeof(T)) % 16 || al % 16 || al4 % (4 * sizeof(T))) return false;
   // value-column slice: the widest with at most 256 threads (one token) / 128 threads
   // (several: more, smaller CTAs to overlap the per-chunk barriers)
-  const int R = d / per, cap = (ntok == 1) ? LA2_DEC1_THREADS : 128;
+  const int R = d / per, cap = (ntok == 1) ? LA2_DEC1_THREADS : LA2_DECT_THREADS;
   int dvc = dv;
   while ((dvc / 4) * R > cap && dvc % 8 == 0) dvc /= 2;
   if ((dvc / 4) * R > cap) return false;
