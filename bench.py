@@ -750,7 +750,9 @@ def extra_workload(args, world, rank, local_rank):
             cb = cpu_reference(N, D, B * H, B * N, B * H)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
             line["cpu_baseline"]["single_core_tokens_per_s"] = B * N / (t_one * B * H)
-        main_dt = "bfloat16" if "bfloat16" in results else "float32"
+        # the config's own dtype: C1 is the reference's fp32 case (BASELINE configs[0]);
+        # its bf16 tensor-core time is reported beside it in per_dtype
+        main_dt = "float32" if w == "c1" else ("bfloat16" if "bfloat16" in results else "float32")
         line.update({"metric": f"{w} fwd+bwd tokens/s", "value": results[main_dt]["tokens_per_s"],
                      "unit": UNIT, "ms_per_step": results[main_dt]["ms_per_step"],
                      "scaling": "strong" if w == "c3" else "weak", "dtype": "bf16" if main_dt == "bfloat16" else "fp32",
