@@ -34,8 +34,31 @@ __device__ __forceinline__ void st_el<__nv_bfloat16>(__nv_bfloat16* p, float x) 
   *p = __float2bfloat16_rn(x);
 }
 
+// Global -> shared staging with U loads in flight per thread before any store (the
+// element-wise loop otherwise waits out one global latency per element): element e of
+// [0, total) is ld(e) -> st(e, value).
+template <int U, typename LD, typename ST>
+__device__ __forceinline__ void stage_batched(int total, int tid, LD ld, ST st) {
+  for (int base = 0; base < total; base += U * SIMT_THREADS) {
+    float r[U];
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const int e = base + w * SIMT_THREADS + tid;
+      r[w] = (e < total) ? ld(e) : 0.f;
+    }
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const int e = base + w * SIMT_THREADS + tid;
+      if (e < total) st(e, r[w]);
+    }
+  }
+}
+
 // Same recurrence and conventions as la2_tc_kernel (see la2_tc.cu), block size 32.
 // One CTA per (b, h, value slice of width <= 64): the state slice is dk x dvs.
+// Register-tiled: 256 threads = 16 x 16; the scores are 2 x 2 tiles, the outputs 2 rows x 4
+// columns, the state fold 4 rows x 4 columns per thread (operands read once per tile from
+// shared memory, rows of V and of the state padded to float4).
 template <typename T, bool REV>
 __global__ void __launch_bounds__(SIMT_THREADS)
     la2_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
@@ -47,16 +70,18 @@ __global__ void __launch_bounds__(SIMT_THREADS)
   const int h = blockIdx.y;
   const int bh = blockIdx.z * p.H + h;
   const int N = p.N;
-  const int ldq = dk + 1, ldv = dv + 1;
-  float* KV = sm;                       // [dk][dv]
-  float* Qs = KV + dk * dv;             // [SB][dk+1]
+  const int ldq = dk + 1;                           // odd: conflict-free column walks
+  const int ldv = (dv + 3) & ~3;                    // float4 rows
+  float* KV = sm;                       // [dk][ldv]
+  float* Qs = KV + dk * ldv;            // [SB][dk+1]
   float* Ks = Qs + SB * ldq;            // [SB][dk+1]
-  float* Vs = Ks + SB * ldq;            // [SB][dv+1]
+  float* Vs = Ks + SB * ldq;            // [SB][ldv]
   float* S = Vs + SB * ldv;             // [SB][SB+1]
   float* pw = S + SB * (SB + 1);        // lam^0 .. lam^SB
   const bool so = (o == nullptr);
 
   const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 thread grid
   if (tid == 0) {
     // iterated products with underflow flush, as tila.power_table
     const float lam = checked_decay(p.decay[h]);
@@ -69,76 +94,141 @@ __global__ void __launch_bounds__(SIMT_THREADS)
     }
   }
   const size_t sbase = static_cast<size_t>(bh) * dk * dvt;
-  for (int e = tid; e < dk * dv; e += SIMT_THREADS) {
-    float x = 0.f;
-    if (p.kv_in != nullptr) {
+  if (p.kv_in != nullptr) {
+    stage_batched<8>(dk * dv, tid, [&](int e) {
       const int c = e / dv, j = e % dv;
-      x = p.kv_in_T ? p.kv_in[sbase + static_cast<size_t>(c0 + j) * dk + c]
-                    : p.kv_in[sbase + static_cast<size_t>(c) * dvt + c0 + j];
-    }
-    KV[e] = x;
+      return p.kv_in_T ? p.kv_in[sbase + static_cast<size_t>(c0 + j) * dk + c]
+                       : p.kv_in[sbase + static_cast<size_t>(c) * dvt + c0 + j];
+    }, [&](int e, float x) { KV[(e / dv) * ldv + e % dv] = x; });
+  } else {
+    for (int e = tid; e < dk * ldv; e += SIMT_THREADS) KV[e] = 0.f;
   }
+  // padding columns of V stay zero (the fold reads whole float4 rows)
+  for (int e = tid; e < SB * ldv; e += SIMT_THREADS) Vs[e] = 0.f;
   const size_t qbase = static_cast<size_t>(bh) * N * dk;
   const size_t vbase = static_cast<size_t>(bh) * N * dvt + c0;
   const int nblk = (N + SB - 1) / SB;
+  const int j0 = 4 * tx;                 // output / fold columns j0 .. j0+3
+  const bool jact = j0 < dv;
   __syncthreads();
 
   for (int i = 0; i < nblk; ++i) {
     const int blk = REV ? (nblk - 1 - i) : i;
     const int t0 = blk * SB;
     const int r = min(SB, N - t0);
-    for (int e = tid; e < SB * dk; e += SIMT_THREADS) {
-      const int t = e / dk, c = e % dk;
-      const bool ok = t < r;
-      if (!so) Qs[t * ldq + c] = ok ? ld_el<T>(q + qbase + static_cast<size_t>(t0 + t) * dk + c) : 0.f;
-      Ks[t * ldq + c] = ok ? ld_el<T>(k + qbase + static_cast<size_t>(t0 + t) * dk + c) : 0.f;
-    }
-    for (int e = tid; e < SB * dv; e += SIMT_THREADS) {
+    // the block's rows (zero past the sequence end); q, k rows are contiguous spans
+    const size_t rbase = qbase + static_cast<size_t>(t0) * dk;
+    if (!so)
+      stage_batched<8>(SB * dk, tid, [&](int e) { return e < r * dk ? ld_el<T>(q + rbase + e) : 0.f; },
+                       [&](int e, float x) { Qs[(e / dk) * ldq + e % dk] = x; });
+    stage_batched<8>(SB * dk, tid, [&](int e) { return e < r * dk ? ld_el<T>(k + rbase + e) : 0.f; },
+                     [&](int e, float x) { Ks[(e / dk) * ldq + e % dk] = x; });
+    stage_batched<8>(SB * dv, tid, [&](int e) {
       const int t = e / dv, j = e % dv;
-      Vs[t * ldv + j] = (t < r) ? ld_el<T>(v + vbase + static_cast<size_t>(t0 + t) * dvt + j) : 0.f;
-    }
+      return (t < r) ? ld_el<T>(v + vbase + static_cast<size_t>(t0 + t) * dvt + j) : 0.f;
+    }, [&](int e, float x) { Vs[(e / dv) * ldv + e % dv] = x; });
     __syncthreads();
     if (!so) {
-      // intra-block scores with the decay mask (lower for forward, upper for reverse)
-      for (int e = tid; e < SB * SB; e += SIMT_THREADS) {
-        const int t = e / SB, u = e % SB;
-        float m = 0.f;
-        if (!REV && u <= t) m = pw[t - u];
-        if (REV && u >= t) m = pw[u - t];
-        float acc = 0.f;
-        if (m != 0.f)
-          for (int c = 0; c < dk; ++c) acc = fmaf(Qs[t * ldq + c], Ks[u * ldq + c], acc);
-        S[t * (SB + 1) + u] = acc * m;
+      // intra-block scores with the decay mask (lower for forward, upper for reverse):
+      // rows 2 ty, 2 ty + 1 x columns 2 tx, 2 tx + 1
+      {
+        const int ta = 2 * ty, ua = 2 * tx;
+        const float* qa = Qs + ta * ldq;
+        const float* ka = Ks + ua * ldq;
+        float s00 = 0.f, s01 = 0.f, s10 = 0.f, s11 = 0.f;
+        const bool live = REV ? (ua + 1 >= ta) : (ua <= ta + 1);  // any unmasked entry
+        if (live) {
+          for (int c = 0; c < dk; ++c) {
+            const float x0 = qa[c], x1 = qa[ldq + c], y0 = ka[c], y1 = ka[ldq + c];
+            s00 = fmaf(x0, y0, s00);
+            s01 = fmaf(x0, y1, s01);
+            s10 = fmaf(x1, y0, s10);
+            s11 = fmaf(x1, y1, s11);
+          }
+        }
+        auto msk = [&](int t, int u) {
+          if (!REV) return (u <= t) ? pw[t - u] : 0.f;
+          return (u >= t) ? pw[u - t] : 0.f;
+        };
+        S[ta * (SB + 1) + ua] = s00 * msk(ta, ua);
+        S[ta * (SB + 1) + ua + 1] = s01 * msk(ta, ua + 1);
+        S[(ta + 1) * (SB + 1) + ua] = s10 * msk(ta + 1, ua);
+        S[(ta + 1) * (SB + 1) + ua + 1] = s11 * msk(ta + 1, ua + 1);
       }
       __syncthreads();
-      for (int e = tid; e < SB * dv; e += SIMT_THREADS) {
-        const int t = e / dv, j = e % dv;
-        if (t >= r) continue;
-        float intra = 0.f;
-        for (int u = 0; u < SB; ++u) intra = fmaf(S[t * (SB + 1) + u], Vs[u * ldv + j], intra);
-        float inter = 0.f;
-        for (int c = 0; c < dk; ++c) inter = fmaf(Qs[t * ldq + c], KV[c * dv + j], inter);
-        const float a = REV ? pw[r - 1 - t] : pw[t + 1];
-        st_el<T>(o + vbase + static_cast<size_t>(t0 + t) * dvt + j, intra + a * inter);
+      // outputs: rows 2 ty, 2 ty + 1 x columns j0 .. j0+3
+      if (jact) {
+        const int ta = 2 * ty;
+        float4 in0 = make_float4(0.f, 0.f, 0.f, 0.f), in1 = in0, it0 = in0, it1 = in0;
+        const float* sa = S + ta * (SB + 1);
+        for (int u = 0; u < SB; ++u) {
+          const float a0 = sa[u], a1 = sa[SB + 1 + u];
+          const float4 b = *reinterpret_cast<const float4*>(Vs + u * ldv + j0);
+          in0.x = fmaf(a0, b.x, in0.x); in0.y = fmaf(a0, b.y, in0.y);
+          in0.z = fmaf(a0, b.z, in0.z); in0.w = fmaf(a0, b.w, in0.w);
+          in1.x = fmaf(a1, b.x, in1.x); in1.y = fmaf(a1, b.y, in1.y);
+          in1.z = fmaf(a1, b.z, in1.z); in1.w = fmaf(a1, b.w, in1.w);
+        }
+        const float* qa = Qs + ta * ldq;
+        for (int c = 0; c < dk; ++c) {
+          const float a0 = qa[c], a1 = qa[ldq + c];
+          const float4 b = *reinterpret_cast<const float4*>(KV + c * ldv + j0);
+          it0.x = fmaf(a0, b.x, it0.x); it0.y = fmaf(a0, b.y, it0.y);
+          it0.z = fmaf(a0, b.z, it0.z); it0.w = fmaf(a0, b.w, it0.w);
+          it1.x = fmaf(a1, b.x, it1.x); it1.y = fmaf(a1, b.y, it1.y);
+          it1.z = fmaf(a1, b.z, it1.z); it1.w = fmaf(a1, b.w, it1.w);
+        }
+        const float in_[2][4] = {{in0.x, in0.y, in0.z, in0.w}, {in1.x, in1.y, in1.z, in1.w}};
+        const float it_[2][4] = {{it0.x, it0.y, it0.z, it0.w}, {it1.x, it1.y, it1.z, it1.w}};
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int t = ta + rr;
+          if (t >= r) continue;
+          const float a = REV ? pw[r - 1 - t] : pw[t + 1];
+          T* op = o + vbase + static_cast<size_t>(t0 + t) * dvt + j0;
+#pragma unroll
+          for (int z = 0; z < 4; ++z)
+            if (j0 + z < dv) st_el<T>(op + z, in_[rr][z] + a * it_[rr][z]);
+        }
       }
       __syncthreads();
     }
-    // state fold: KV <- lam^r KV + sum_u w_u k_u^T v_u
-    const float fr = pw[r];
-    for (int e = tid; e < dk * dv; e += SIMT_THREADS) {
-      const int c = e / dv, j = e % dv;
-      float acc = 0.f;
-      for (int u = 0; u < r; ++u) {
-        const float w = REV ? pw[u + 1] : pw[r - 1 - u];
-        acc = fmaf(w * Ks[u * ldq + c], Vs[u * ldv + j], acc);
+    // state fold: KV <- lam^r KV + sum_u w_u k_u^T v_u; thread tile: rows 4 g .. 4 g + 3
+    // (g = ty, ty + 16, ...) x columns j0 .. j0 + 3
+    if (jact) {
+      const float fr = pw[r];
+      for (int g = ty; 4 * g < dk; g += 16) {
+        const int cr = 4 * g;
+        float4 acc[4];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) acc[z] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < r; ++u) {
+          const float w = REV ? pw[u + 1] : pw[r - 1 - u];
+          const float4 b = *reinterpret_cast<const float4*>(Vs + u * ldv + j0);
+          const float* ku = Ks + u * ldq + cr;
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            const float a = (cr + z < dk) ? w * ku[z] : 0.f;
+            acc[z].x = fmaf(a, b.x, acc[z].x); acc[z].y = fmaf(a, b.y, acc[z].y);
+            acc[z].z = fmaf(a, b.z, acc[z].z); acc[z].w = fmaf(a, b.w, acc[z].w);
+          }
+        }
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          if (cr + z >= dk) break;
+          float4* kvp = reinterpret_cast<float4*>(KV + (cr + z) * ldv + j0);
+          float4 x = *kvp;
+          x.x = fmaf(fr, x.x, acc[z].x); x.y = fmaf(fr, x.y, acc[z].y);
+          x.z = fmaf(fr, x.z, acc[z].z); x.w = fmaf(fr, x.w, acc[z].w);
+          *kvp = x;
+        }
       }
-      KV[e] = fmaf(fr, KV[e], acc);
     }
     __syncthreads();
   }
   if (p.kv_out != nullptr)
     for (int e = tid; e < dk * dv; e += SIMT_THREADS)
-      p.kv_out[sbase + static_cast<size_t>(e / dv) * dvt + c0 + e % dv] = KV[e];
+      p.kv_out[sbase + static_cast<size_t>(e / dv) * dvt + c0 + e % dv] = KV[(e / dv) * ldv + e % dv];
 }
 
 int launch_simt(const FArgs& a, cudaStream_t st) {
@@ -155,8 +245,9 @@ int launch_simt(const FArgs& a, cudaStream_t st) {
   p.kv_in_T = a.kv_in_T;
   p.kv_out = a.kv_out;
   p.dv_total = a.dv;
-  const size_t smem = sizeof(float) * (static_cast<size_t>(a.dk) * dvs + 2 * SB * (a.dk + 1) +
-                                       SB * (dvs + 1) + SB * (SB + 1) + SB + 1);
+  const size_t ldv = (dvs + 3) & ~3;
+  const size_t smem = sizeof(float) * (static_cast<size_t>(a.dk) * ldv + 2 * SB * (a.dk + 1) +
+                                       SB * ldv + SB * (SB + 1) + SB + 1);
   dim3 grid(nslices, a.H, a.B);
   cudaError_t e;
 #define LA2_SIMT_LAUNCH(TY, RV)                                                                   \
@@ -533,28 +624,46 @@ struct ScanLens {
   int len[64];
 };
 
+// The chunk factors lam^len_g depend only on (head, g): they are computed once per CTA
+// into shared memory (double-precision exp2, as before, so the values are unchanged) for
+// the head of the CTA's first element; an element of another head (a CTA straddling two
+// heads) computes its own. Loads run 8 chunks ahead of the serial combine.
 __global__ void la2_scan_kernel(const float* __restrict__ states, const float* __restrict__ decay,
                                 const float* __restrict__ init, float* __restrict__ out, int G,
                                 int BH, int H, int per, ScanLens lens, int reverse) {
+  __shared__ float fac[64];
   const size_t total = static_cast<size_t>(BH) * per;
-  const size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t first = static_cast<size_t>(blockIdx.x) * blockDim.x;
+  const int bh0 = static_cast<int>(first / per);
+  auto factor = [&](int bh, int g) {
+    const double l2 = log2(static_cast<double>(checked_decay(decay[bh % H])));
+    float f = static_cast<float>(exp2(l2 * lens.len[g]));
+    return (f < 1.17549435e-38f) ? 0.f : f;
+  };
+  if (threadIdx.x < G) fac[threadIdx.x] = factor(bh0, threadIdx.x);
+  __syncthreads();
+  const size_t e = first + threadIdx.x;
   if (e >= total) return;
   const int bh = static_cast<int>(e / per);
-  const double l2 = log2(static_cast<double>(checked_decay(decay[bh % H])));
+  const bool own = (bh == bh0);
   float acc = init ? init[e] : 0.f;
-  if (!reverse) {
-    for (int g = 0; g < G; ++g) {
-      out[static_cast<size_t>(g) * total + e] = acc;
-      float f = static_cast<float>(exp2(l2 * lens.len[g]));
-      if (f < 1.17549435e-38f) f = 0.f;
-      acc = fmaf(f, acc, states[static_cast<size_t>(g) * total + e]);
+  constexpr int U = 8;
+  for (int g0 = 0; g0 < G; g0 += U) {
+    float x[U];
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const int gi = g0 + w;
+      const int g = reverse ? G - 1 - gi : gi;
+      x[w] = (gi < G) ? states[static_cast<size_t>(g) * total + e] : 0.f;
     }
-  } else {
-    for (int g = G - 1; g >= 0; --g) {
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const int gi = g0 + w;
+      if (gi >= G) break;
+      const int g = reverse ? G - 1 - gi : gi;
       out[static_cast<size_t>(g) * total + e] = acc;
-      float f = static_cast<float>(exp2(l2 * lens.len[g]));
-      if (f < 1.17549435e-38f) f = 0.f;
-      acc = fmaf(f, acc, states[static_cast<size_t>(g) * total + e]);
+      const float f = own ? fac[g] : factor(bh, g);
+      acc = fmaf(f, acc, x[w]);
     }
   }
 }

@@ -124,6 +124,31 @@ def _check_cuda_decay(d: torch.Tensor, src: Optional[torch.Tensor] = None) -> No
     _CHECKED[id(owner)] = (weakref.ref(owner), stamp)
 
 
+_REPEAT: dict = {}
+
+
+def decay_repeat(dec: torch.Tensor, g: int) -> torch.Tensor:
+    """``dec.repeat_interleave(g)`` for the g-way sequence split (head h's chunks are heads
+    h*g .. h*g+g-1), cached per (validated decay tensor, version, g): the split path would
+    otherwise build a fresh tensor per op, and a fresh CUDA decay tensor costs one
+    validation -- a stream synchronization -- per call. The result inherits ``dec``'s
+    validation."""
+    key = (id(dec), g)
+    stamp = (dec.data_ptr(), dec._version)
+    hit = _REPEAT.get(key)
+    if hit is not None and hit[0]() is dec and hit[1] == stamp:
+        return hit[2]
+    if dec.is_cuda:
+        _check_cuda_decay(dec)
+    r = dec.repeat_interleave(g)
+    _CHECKED[id(r)] = (weakref.ref(r), (r.data_ptr(), r._version))
+    if len(_REPEAT) >= 1024:
+        for k_ in [k_ for k_, (w, _, _) in _REPEAT.items() if w() is None]:
+            del _REPEAT[k_]
+    _REPEAT[key] = (weakref.ref(dec), stamp, r)
+    return r
+
+
 def _decay(decay: DecayLike, H: int, device: torch.device, dtype=torch.float32) -> torch.Tensor:
     """decay_tensor for the ops' own use: host values (lists, floats, CPU tensors) are
     validated and uploaded once per distinct (values, device) and the device copy is
@@ -242,7 +267,7 @@ def split_forward(q, k, v, decay, g: int, kv_in=None, output_final_state=False):
     ``(o, kv_out, prefix)``; prefix (chunk-carried states) is reused by the backward."""
     B, H, N, d, dv = _check_qkv(q, k, v)
     dec = _decay(decay, H, q.device)
-    dec_g = dec.repeat_interleave(g)
+    dec_g = decay_repeat(dec, g)
     q4, k4, v4 = _chunked(q.contiguous(), g), _chunked(k.contiguous(), g), _chunked(v.contiguous(), g)
     s = chunk_state(k4, v4, dec_g)
     init = None if kv_in is None else _state(kv_in, B, H, d, dv, q.device, "kv_in")
@@ -257,7 +282,7 @@ def split_backward(q, k, v, d_out, decay, g: int, prefix, dkv_in=None, output_dk
     B, H, N, d, dv = _check_qkv(q, k, v)
     _on(q.device, d_out=d_out)
     dec = _decay(decay, H, q.device)
-    dec_g = dec.repeat_interleave(g)
+    dec_g = decay_repeat(dec, g)
     q4, k4, v4, do4 = (_chunked(t.contiguous(), g) for t in (q, k, v, d_out))
     t = chunk_dstate(q4, do4, dec_g)
     init = None if dkv_in is None else _state(dkv_in, B, H, d, dv, q.device, "dkv_in")

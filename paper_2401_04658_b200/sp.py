@@ -65,7 +65,7 @@ def cuda_ops(seq_split="auto") -> LocalOps:
         g = st["g"] = factor(B, H, L, d, dv, k.dtype)
         if g == 1:
             return ops.chunk_state(k, v, dec)
-        dec_g = dec.repeat_interleave(g)
+        dec_g = ops.decay_repeat(dec, g)
         s = ops.chunk_state(ops._chunked(k.contiguous(), g), ops._chunked(v.contiguous(), g), dec_g)
         s5 = st["s5"] = ops._to_chunk_major(s, B, H, g)
         pre = ops.state_scan(s5, dec, [L // g] * g)
@@ -78,7 +78,7 @@ def cuda_ops(seq_split="auto") -> LocalOps:
             return ops.la2_forward(q, k, v, dec, kv_in=kv_in)[0]
         prefix = ops._from_chunk_major(ops.state_scan(st["s5"], dec, [L // g] * g, init=kv_in), B, H, g)
         q4, k4, v4 = (ops._chunked(t.contiguous(), g) for t in (q, k, v))
-        o4, _ = ops.la2_forward(q4, k4, v4, dec.repeat_interleave(g), kv_in=prefix)
+        o4, _ = ops.la2_forward(q4, k4, v4, ops.decay_repeat(dec, g), kv_in=prefix)
         return o4.view(B, H, L, v.shape[3])
 
     def chunk_dstate(q, do, dec):
@@ -88,7 +88,7 @@ def cuda_ops(seq_split="auto") -> LocalOps:
         if g == 1:
             return ops.chunk_dstate(q, do, dec)
         t = ops.chunk_dstate(ops._chunked(q.contiguous(), g), ops._chunked(do.contiguous(), g),
-                             dec.repeat_interleave(g))
+                             ops.decay_repeat(dec, g))
         t5 = st["t5"] = ops._to_chunk_major(t, B, H, g)
         suf = ops.state_scan(t5, dec, [L // g] * g, reverse=True)
         return _decay_pow(dec, torch.tensor(L // g)) * suf[0] + t5[0]
@@ -106,7 +106,7 @@ def cuda_ops(seq_split="auto") -> LocalOps:
         suffix = ops._from_chunk_major(ops.state_scan(st["t5"], dec, lens, init=dkv_in, reverse=True),
                                        B, H, g)
         q4, k4, v4, do4 = (ops._chunked(t.contiguous(), g) for t in (q, k, v, do))
-        dq, dk, dvv, _ = ops.la2_backward(q4, k4, v4, do4, dec.repeat_interleave(g), kv_in=prefix,
+        dq, dk, dvv, _ = ops.la2_backward(q4, k4, v4, do4, ops.decay_repeat(dec, g), kv_in=prefix,
                                           dkv_in=suffix)
         return dq.view(B, H, L, d), dk.view(B, H, L, d), dvv.view(B, H, L, dv)
 
