@@ -36,6 +36,11 @@ pytestmark = pytest.mark.gpu
     ("memcheck", "2,3,19,128,t"),
     ("racecheck", "2,3,19,128,t"),
     ("initcheck", "1,2,11,64,t"),
+    # fp32 on the register-tiled SIMT kernels: split path (chunk states, scans) and raw passes,
+    # a partial last block and a width that is not a multiple of 4
+    ("memcheck", "1,3,1000,64,f"),
+    ("racecheck", "1,2,300,20,f"),
+    ("initcheck", "1,2,300,20,f"),
 ])
 def test_sanitizer_clean(tool, shape):
     if not os.path.exists(SAN):
