@@ -739,6 +739,43 @@ def test_mixed_device_arguments_refused():
     assert torch.isfinite(o.float()).all()
 
 
+def test_no_decay_revalidation_in_steady_state(monkeypatch):
+    """A CUDA decay tensor is validated once (la2_check_decay synchronizes the stream);
+    after the first step no path -- stored-state triple, d = 128 replay, bf16 and fp32
+    sequence split, decode -- validates again (a per-op re-validation of the split's
+    per-chunk decay once cost C5 12 %)."""
+    from paper_2401_04658_b200 import _lib
+    calls = []
+    orig = _lib.call
+
+    def spy(name, *args):
+        if name.startswith("la2_check_decay"):
+            calls.append(name)
+        return orig(name, *args)
+
+    monkeypatch.setattr(_lib, "call", spy)
+    cases = [((1, 2, 16384, 64), torch.bfloat16), ((1, 2, 4096, 128), torch.bfloat16),
+             ((1, 2, 65536, 64), torch.bfloat16), ((1, 8, 2048, 64), torch.float32)]
+    for (B, H, N, D), dt in cases:
+        q, k, v, do = gpu(*inputs(B, H, N, D, D, dt, seed=N))
+        dec = la2.decay_tensor(list(np.linspace(0.9, 1.0, H)), H, torch.device(DEV))
+
+        def step():
+            qg, kg, vg = (t.clone().requires_grad_() for t in (q, k, v))
+            la2.lightning_attn2(qg, kg, vg, dec).backward(do)
+
+        calls.clear()
+        step()
+        assert calls, "the spy sees the first (fresh tensor) validation"
+        calls.clear()
+        step()
+        st = torch.zeros(B, H, D, D, device=DEV)
+        la2.decode_step(q[:, :, 0], k[:, :, 0], v[:, :, 0], dec, st)
+        la2.decode_tokens(q[:, :, :5], k[:, :, :5], v[:, :, :5], dec, st)
+        torch.cuda.synchronize()
+        assert not calls, ((B, H, N, D, dt), calls)
+
+
 def test_concurrent_backward_and_graph_capture():
     """The dQ scan on a forked side stream gives bitwise the same gradients as the serial
     order, and the fork/join is capturable in a CUDA graph (replay == eager)."""
