@@ -9,7 +9,7 @@ for (B, H, N, D) in [(1, 8, 2048, 64), (1, 8, 8192, 64), (1, 8, 1024, 64), (1, 1
     q, k, v, do = ((torch.rand(B, H, N, D, device=dev) * 2 - 1) for _ in range(4))
     dec = ([0.5, 0.8, 0.9, 0.95, 0.99, 0.999, 0.9999, 1.0] * 2)[:H]
     print(B, H, N, D, "auto split", la2.split_factor(B, H, N, D, D, torch.float32))
-    for g in ["auto", 8, 16, 32, 64]:
+    for g in ["auto", 1, 4, 8, 16, 32, 64]:
         if g != "auto" and N % g:
             continue
         def step():
