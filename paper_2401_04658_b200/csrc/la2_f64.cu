@@ -28,6 +28,9 @@ __device__ __forceinline__ double checked_decay64(double lam) {
 
 // One CTA per (b, h, value slice of <= FDV columns); the dk x dvs state lives in smem.
 // kv_in: [B,H,dk,dv] (kv_in_T: stored [B,H,dv,dk]); kv_out: [B,H,dk,dv].
+// 256 threads as 16 x 16, register-tiled: a score per thread, 1 x 2 outputs, 4 x 2 state
+// entries (per group of 64 state rows) -- every output keeps the sequential fma order of
+// the element-wise formulation, so the results are unchanged bit for bit.
 template <bool REV>
 __global__ void __launch_bounds__(F64_THREADS)
     la2_f64_kernel(const double* __restrict__ q, const double* __restrict__ k, const double* __restrict__ v,
@@ -38,14 +41,16 @@ __global__ void __launch_bounds__(F64_THREADS)
   const int dv = min(FDV, dvt - c0);
   const int h = blockIdx.y;
   const int bh = blockIdx.z * H + h;
-  const int ldq = dk + 1, ldv = dv + 1;
-  double* KV = smd;                    // [dk][dv]
-  double* Qs = KV + dk * dv;           // [FB][dk+1]
+  const int ldq = dk + 1;
+  constexpr int LDV = FDV;             // V and state rows padded to the slice width
+  double* KV = smd;                    // [dk][LDV]
+  double* Qs = KV + dk * LDV;          // [FB][dk+1]
   double* Ks = Qs + FB * ldq;          // [FB][dk+1]
-  double* Vs = Ks + FB * ldq;          // [FB][dv+1]
-  double* S = Vs + FB * ldv;           // [FB][FB+1]
+  double* Vs = Ks + FB * ldq;          // [FB][LDV]
+  double* S = Vs + FB * LDV;           // [FB][FB+1]
   double* pw = S + FB * (FB + 1);      // lam^0 .. lam^FB
   const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
   if (tid == 0) {
     const double lam = checked_decay64(decay[h]);
     double acc = 1.0;
@@ -57,18 +62,19 @@ __global__ void __launch_bounds__(F64_THREADS)
     }
   }
   const size_t sbase = static_cast<size_t>(bh) * dk * dvt;
-  for (int e = tid; e < dk * dv; e += F64_THREADS) {
+  for (int e = tid; e < dk * LDV; e += F64_THREADS) {
+    const int c = e / LDV, j = e % LDV;
     double x = 0.0;
-    if (kv_in != nullptr) {
-      const int c = e / dv, j = e % dv;
+    if (kv_in != nullptr && j < dv)
       x = kv_in_T ? kv_in[sbase + static_cast<size_t>(c0 + j) * dk + c]
                   : kv_in[sbase + static_cast<size_t>(c) * dvt + c0 + j];
-    }
     KV[e] = x;
   }
+  for (int e = tid; e < FB * LDV; e += F64_THREADS) Vs[e] = 0.0;
   const size_t qbase = static_cast<size_t>(bh) * N * dk;
   const size_t vbase = static_cast<size_t>(bh) * N * dvt + c0;
   const int nblk = (N + fb - 1) / fb;
+  const int j0 = 2 * tx;  // output / state columns j0, j0 + 1
   __syncthreads();
   for (int i = 0; i < nblk; ++i) {
     const int blk = REV ? (nblk - 1 - i) : i;
@@ -82,12 +88,12 @@ __global__ void __launch_bounds__(F64_THREADS)
     }
     for (int e = tid; e < fb * dv; e += F64_THREADS) {
       const int t = e / dv, j = e % dv;
-      Vs[t * ldv + j] = (t < r) ? v[vbase + static_cast<size_t>(t0 + t) * dvt + j] : 0.0;
+      Vs[t * LDV + j] = (t < r) ? v[vbase + static_cast<size_t>(t0 + t) * dvt + j] : 0.0;
     }
     __syncthreads();
     // intra-block scores with the decay mask (lower for the forward scan, upper reversed)
-    for (int e = tid; e < fb * fb; e += F64_THREADS) {
-      const int t = e / fb, u = e % fb;
+    if (ty < fb && tx < fb) {
+      const int t = ty, u = tx;
       double m = 0.0;
       if (!REV && u <= t) m = pw[t - u];
       if (REV && u >= t) m = pw[u - t];
@@ -97,33 +103,60 @@ __global__ void __launch_bounds__(F64_THREADS)
       S[t * (FB + 1) + u] = acc * m;
     }
     __syncthreads();
-    for (int e = tid; e < fb * dv; e += F64_THREADS) {
-      const int t = e / dv, j = e % dv;
-      if (t >= r) continue;
-      double intra = 0.0;
-      for (int u = 0; u < fb; ++u) intra = fma(S[t * (FB + 1) + u], Vs[u * ldv + j], intra);
-      double inter = 0.0;
-      for (int c = 0; c < dk; ++c) inter = fma(Qs[t * ldq + c], KV[c * dv + j], inter);
+    if (ty < r && j0 < dv) {
+      const int t = ty;
+      double in0 = 0.0, in1 = 0.0, it0 = 0.0, it1 = 0.0;
+      for (int u = 0; u < fb; ++u) {
+        const double a = S[t * (FB + 1) + u];
+        const double2 b = *reinterpret_cast<const double2*>(Vs + u * LDV + j0);
+        in0 = fma(a, b.x, in0);
+        in1 = fma(a, b.y, in1);
+      }
+      for (int c = 0; c < dk; ++c) {
+        const double a = Qs[t * ldq + c];
+        const double2 b = *reinterpret_cast<const double2*>(KV + c * LDV + j0);
+        it0 = fma(a, b.x, it0);
+        it1 = fma(a, b.y, it1);
+      }
       const double a = REV ? pw[r - 1 - t] : pw[t + 1];
-      o[vbase + static_cast<size_t>(t0 + t) * dvt + j] = intra + a * inter;
+      double* op = o + vbase + static_cast<size_t>(t0 + t) * dvt + j0;
+      op[0] = in0 + a * it0;
+      if (j0 + 1 < dv) op[1] = in1 + a * it1;
     }
     __syncthreads();
-    // state fold: KV <- lam^r KV + sum_u w_u k_u^T v_u
-    const double fr = pw[r];
-    for (int e = tid; e < dk * dv; e += F64_THREADS) {
-      const int c = e / dv, j = e % dv;
-      double acc = 0.0;
-      for (int u = 0; u < r; ++u) {
-        const double w = REV ? pw[u + 1] : pw[r - 1 - u];
-        acc = fma(w * Ks[u * ldq + c], Vs[u * ldv + j], acc);
+    // state fold: KV <- lam^r KV + sum_u w_u k_u^T v_u (rows 4 g .. 4 g + 3, g = ty, ty+16, ...)
+    if (j0 < dv) {
+      const double fr = pw[r];
+      for (int g = ty; 4 * g < dk; g += 16) {
+        const int cr = 4 * g;
+        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        for (int u = 0; u < r; ++u) {
+          const double w = REV ? pw[u + 1] : pw[r - 1 - u];
+          const double2 b = *reinterpret_cast<const double2*>(Vs + u * LDV + j0);
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            if (cr + z < dk) {
+              const double a = w * Ks[u * ldq + cr + z];
+              acc[z][0] = fma(a, b.x, acc[z][0]);
+              acc[z][1] = fma(a, b.y, acc[z][1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          if (cr + z < dk) {
+            double* kv = KV + (cr + z) * LDV + j0;
+            kv[0] = fma(fr, kv[0], acc[z][0]);
+            kv[1] = fma(fr, kv[1], acc[z][1]);
+          }
+        }
       }
-      KV[e] = fma(fr, KV[e], acc);
     }
     __syncthreads();
   }
   if (kv_out != nullptr)
     for (int e = tid; e < dk * dv; e += F64_THREADS)
-      kv_out[sbase + static_cast<size_t>(e / dv) * dvt + c0 + e % dv] = KV[e];
+      kv_out[sbase + static_cast<size_t>(e / dv) * dvt + c0 + e % dv] = KV[(e / dv) * LDV + e % dv];
 }
 
 int launch_f64(const double* q, const double* k, const double* v, double* o, const double* decay,
@@ -142,8 +175,9 @@ int launch_f64(const double* q, const double* k, const double* v, double* o, con
   }
   const int dvs = dv < FDV ? dv : FDV;
   const int nslices = (dv + FDV - 1) / FDV;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(dk) * dvs + 2 * FB * (dk + 1) +
-                                        FB * (dvs + 1) + FB * (FB + 1) + FB + 1);
+  (void)dvs;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(dk) * FDV + 2 * FB * (dk + 1) +
+                                        FB * FDV + FB * (FB + 1) + FB + 1);
   const dim3 grid(nslices, H, B);
   auto kern = reverse ? la2_f64_kernel<true> : la2_f64_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
