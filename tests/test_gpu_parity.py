@@ -389,6 +389,23 @@ def test_decode_tokens_equals_single_steps_bitwise(dtype, d, dv):
         assert rel(oT, ref) <= tol and rel(stT, S) <= max(tol, 1e-6)
 
 
+def test_decode_tokens_edges():
+    """T = 0 is a no-op (state untouched); recurrent_forward from a given state equals the
+    forward with kv_in; fp32 multi-token decode matches the fp64 recurrence."""
+    B, H, D = 2, 3, 64
+    decay = [0.5, 0.99, 1.0]
+    st = torch.rand(B, H, D, D, device=DEV)
+    st0 = st.clone()
+    e = torch.empty(B, H, 0, D, device=DEV, dtype=torch.bfloat16)
+    o = la2.decode_tokens(e, e, e, decay, st)
+    assert o.shape == (B, H, 0, D) and torch.equal(st, st0)
+    q, k, v, _ = gpu(*inputs(B, H, 40, D, D, torch.float32, seed=9))
+    o_r, st_r = la2.recurrent_forward(q, k, v, decay, initial_state=st0)
+    o_f, st_f = la2.la2_forward(q, k, v, decay, kv_in=st0, output_final_state=True)
+    assert torch.equal(st0, st)  # the initial state is not modified
+    assert rel(o_r, to64(o_f)) <= FP32_TOL and rel(st_r, to64(st_f)) <= FP32_TOL
+
+
 def test_recurrent_forward_against_reference_golden(golden):
     """GPU per-token recurrence (one la2_decode_tokens_f64 launch) vs the reference's own
     tila.recurrent_forward outputs on its grid (golden.npz, fp64) and the tiled final
