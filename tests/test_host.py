@@ -226,3 +226,24 @@ def test_bench_reference_arm_contract():
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def test_missing_library_fails_loudly():
+    """Without the built library the ops raise ImportError ("no CPU fallback") instead of
+    computing anything on the host."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = ("import paper_2401_04658_b200 as la2\n"
+            "from paper_2401_04658_b200 import _lib\n"
+            "try:\n"
+            "    _lib.load()\n"
+            "except ImportError as e:\n"
+            "    print('ImportError:', e)\n")
+    env = dict(os.environ, LA2_LIB=str(root / "does_not_exist" / "libla2.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ImportError" in r.stdout and "no CPU fallback" in r.stdout, (r.stdout, r.stderr)
