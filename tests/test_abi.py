@@ -172,3 +172,11 @@ def test_tensor_core_envelope_documented():
     text = HEADER.read_text()
     assert "multiples of 8 up to 256" in text
     assert "la2_forward_f64" in text and "la2_backward_f64" in text
+
+
+def test_integration_table_covers_header():
+    """INTEGRATION.md names every entry point include/la2.h declares (with the reference
+    function it replaces, or why it has none)."""
+    text = (HEADER.parents[1] / "INTEGRATION.md").read_text()
+    missing = [s for s in declared_symbols() if f"`{s}`" not in text and f"{s}`" not in text]
+    assert not missing, missing
